@@ -1,0 +1,191 @@
+/*
+ * lamb.h — C ABI of the B200-native sharded LAMB step (ABI v1).
+ *
+ * What this library computes is the data-parallel hot path of MegaScale (arXiv 2402.15627):
+ *   - the LAMB optimizer the paper adopts to grow the batch 4x (§3.1 P:288-293,
+ *     citing You et al. 2020 `You2020Large`; update rule = that paper's Algorithm 2,
+ *     readings Z1-Z9 in DESIGN.md §3),
+ *   - on ZeRO-2 data parallelism: gradients reduce-scattered, optimizer state sharded,
+ *     parameters all-gathered (§2, Fig. fig:dp-zero; §3.2).
+ * One lamb_step = (a1) reduce-scatter of bf16 gradients with fp32 accumulation, (a2) Adam
+ * moments + update vector on the local shard, (a3) segmented per-tensor ||w||^2, ||u||^2 and
+ * their cross-shard combine, (a4) trust ratio, (a5) w <- w - lr*ratio*u and the bf16 cast,
+ * (a6) all-gather of the bf16 parameters.
+ *
+ * Conventions (all functions):
+ *   - Return LAMB_OK or an error code; lamb_last_error(h) (h may be NULL) holds a message.
+ *   - Pointers are plain host or device pointers as stated per argument.  `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Collective calls (marked COLLECTIVE) must be made by all world_size ranks with
+ *     identical tensor/group tables, config (except rank/device) and step.
+ *   - One handle is not thread-safe; several handles per process are allowed.
+ *   - There is no CPU fallback: a device that is not sm_100 gives LAMB_EUNSUPPORTED.
+ */
+#ifndef LAMB_H_
+#define LAMB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAMB_ABI_VERSION 1
+#define LAMB_MAX_GROUPS 64      /* hyper-parameter groups per handle */
+#define LAMB_MAX_RANKS 8        /* ranks of one NVSwitch node */
+#define LAMB_UNIQUE_ID_BYTES 128
+
+typedef struct lamb_ctx* lamb_t;          /* one per (rank, device, parameter set) */
+typedef struct lamb_plan_ctx* lamb_plan_t;
+
+typedef enum {
+    LAMB_OK = 0,
+    LAMB_EINVAL = 1,        /* bad argument (see each function) */
+    LAMB_ENOMEM = 2,        /* device or host allocation failed */
+    LAMB_ECUDA = 3,         /* CUDA runtime error (incl. asynchronous faults, barrier timeout) */
+    LAMB_ENCCL = 4,         /* NCCL error */
+    LAMB_ESTATE = 5,        /* call out of order (e.g. lamb_step before the master is set) */
+    LAMB_EUNSUPPORTED = 6   /* not an sm_100 device, unsupported mode or feature */
+} lamb_status;
+
+/* Parameter-tensor table row ("layer" = one tensor, reading Z2).  numel >= 1. */
+typedef struct {
+    int64_t numel;
+    int32_t group;          /* index into the group table */
+    int32_t reserved;       /* must be 0 */
+} lamb_tensor;
+
+/* Hyper-parameter group.  The fp32 values ARE the contract (reading Z6).
+ * beta1, beta2 in [0,1); eps >= 0; lr >= 0; weight_decay >= 0.
+ * adapt = 1: LAMB trust ratio ||w||/||u|| (fallback 1 on a zero norm, Z9);
+ * adapt = 0: ratio 1 (exactly AdamW, Z8).  bias_correction = 1: Adam bias correction (Z5). */
+typedef struct {
+    float lr, beta1, beta2, eps, weight_decay;
+    int32_t adapt, bias_correction;
+} lamb_group;
+
+/* comm_mode */
+#define LAMB_COMM_NCCL 0     /* baseline: NCCL reduce-scatter(fp32)/all-gather(fp64)/all-gather(bf16) */
+#define LAMB_COMM_FUSED 1    /* default: reduce-scatter fused into pass A (NVLink peer loads,
+                                fp32 sum), all-gather fused into pass B (NVLink peer stores) */
+/* flags */
+#define LAMB_FLAG_TIMING 1   /* record CUDA events around every phase (lamb_timing_*) */
+
+typedef struct {
+    int32_t world_size;        /* D >= 1, <= LAMB_MAX_RANKS; D = 1 needs no unique id */
+    int32_t rank;              /* [0, D) */
+    int32_t device;            /* CUDA device ordinal of this rank */
+    int32_t comm_mode;         /* LAMB_COMM_*; ignored at D = 1 */
+    int64_t bucket_cap_elems;  /* bucket cap (rule P3); 0 -> 40,000,000 */
+    float grad_scale;          /* reduced gradient = grad_scale * sum_j G_j; 0 -> 1/D (Z10) */
+    int32_t flags;             /* LAMB_FLAG_* */
+} lamb_config;
+
+/* Read-only views of the shard/bucket plan (row a0, rules P1-P7 in DESIGN.md §2).
+ * All tables are int64, host memory owned by the handle, valid until destroy. */
+typedef struct {
+    int64_t n_tensors, n_buckets, n_segments, n_straddlers;
+    int64_t flat_size;          /* elements of the flat bf16 grad / param buffers */
+    int64_t shard_size;         /* elements of this rank's fp32 w/m/v shard = flat_size / D */
+    int32_t world_size, rank;
+    const int64_t* tensor_off;      /* [n_tensors] flat offset of each tensor (8-aligned, P2) */
+    const int64_t* tensor_bucket;   /* [n_tensors] */
+    const int64_t* buckets;         /* [n_buckets][4] = {base, S_b, t_begin, t_end} (P3-P5) */
+    const int64_t* segments;        /* [n_segments][4] = {tensor, shard_off, tensor_off, len}
+                                       of THIS rank, shard order (P6-P7) */
+    const int64_t* straddlers;      /* [n_straddlers] tensors with >= 2 segments, ascending */
+} lamb_plan_view;
+
+/* ---------------- host-only planner (row a0; no device needed) ---------------- */
+/* Builds the plan of `rank` for a world of `world_size`.  cap = 0 -> 40,000,000.
+ * EINVAL: n_tensors < 1, numel < 1, world_size not in [1, LAMB_MAX_RANKS], rank out of range,
+ * cap < 0. */
+lamb_status lamb_plan_create(const lamb_tensor* tensors, int64_t n_tensors, int32_t world_size,
+                             int32_t rank, int64_t cap, lamb_plan_t* out);
+lamb_status lamb_plan_get(lamb_plan_t plan, lamb_plan_view* out);
+void lamb_plan_destroy(lamb_plan_t plan);
+
+/* ---------------- lifecycle ---------------- */
+/* Rank 0 creates the NCCL unique id; the caller broadcasts the 128 bytes (torch.distributed). */
+lamb_status lamb_get_unique_id(uint8_t id[LAMB_UNIQUE_ID_BYTES]);
+
+/* COLLECTIVE.  Plans, allocates (library-owned: flat bf16 grad and param buffers, zeroed;
+ * fp32 w/m/v shards), creates the NCCL communicator and, in LAMB_COMM_FUSED, maps every
+ * peer's grad/param/exchange buffers over NVLink (CUDA IPC).  `id` may be NULL when D = 1.
+ * EINVAL: see lamb_plan_create, n_groups not in [1, LAMB_MAX_GROUPS], group out of range,
+ * bad hyper-parameters, reserved != 0.  ENOMEM, ECUDA, ENCCL, EUNSUPPORTED (device not
+ * sm_100, or peers not NVLink-reachable in FUSED mode). */
+lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors, const lamb_group* groups,
+                        int32_t n_groups, const lamb_config* cfg,
+                        const uint8_t id[LAMB_UNIQUE_ID_BYTES], lamb_t* out);
+
+/* COLLECTIVE, asynchronous, stream-ordered on `stream`.  Gradients are read from the
+ * library grad buffer (lamb_buffer(LAMB_BUF_GRAD)) — every rank holds its full flat bf16
+ * gradient there, padding elements zero — or, when `grads` != NULL (D = 1 or NCCL mode),
+ * from a caller-owned device buffer with the same layout.  When `stream` reaches the end of
+ * the step: every rank's param buffer holds bf16_rne(w) of the updated params, each shard
+ * holds the updated fp32 w, m, v.  No host synchronisation.  step >= 1 is LAMB's t.
+ * EINVAL: step < 1, grads != NULL in FUSED mode with D > 1.  ESTATE: master not set.
+ * ECUDA/ENCCL: launch failures or an asynchronous fault/timeout of an earlier step. */
+lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void* stream);
+
+/* COLLECTIVE.  End-to-end variant with HOST buffers: copies `host_grads` (flat bf16,
+ * flat_size elements, pinned for full speed) into the grad buffer, runs lamb_step, and
+ * copies the full updated bf16 param buffer back into `host_params` (flat_size elements).
+ * Stream-ordered; the caller synchronises `stream` before reading host_params. */
+lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_params,
+                           int64_t step, void* stream);
+
+/* COLLECTIVE (barrier-free teardown of this rank's peer mappings and communicator). */
+void lamb_destroy(lamb_t h);
+
+/* ---------------- queries, state, hooks ---------------- */
+lamb_status lamb_query_plan(lamb_t h, lamb_plan_view* out);
+
+#define LAMB_BUF_GRAD 0    /* bf16 [flat_size], caller writes gradients here */
+#define LAMB_BUF_PARAM 1   /* bf16 [flat_size], updated params after each step */
+#define LAMB_BUF_W 2       /* fp32 [shard_size] master weights, shard-local order */
+#define LAMB_BUF_M 3       /* fp32 [shard_size] first moment (stored uncorrected, Z5) */
+#define LAMB_BUF_V 4       /* fp32 [shard_size] second moment */
+/* Device pointer + element count of a library buffer; valid until lamb_destroy. */
+lamb_status lamb_buffer(lamb_t h, int32_t which, void** dev_ptr, int64_t* n_elems);
+
+/* Sets the fp32 master from a FULL flat fp32 array (flat_size elements, plan layout,
+ * padding 0; host memory if on_device = 0): copies this rank's slices into w, zeroes m and
+ * v, writes bf16_rne into the whole param buffer.  Synchronous w.r.t. `stream`. */
+lamb_status lamb_set_master(lamb_t h, const float* full_flat, int32_t on_device, void* stream);
+
+/* Copies this rank's shard of W/M/V (LAMB_BUF_W/M/V; shard_size floats, shard order) to
+ * dst (host if on_device = 0).  Synchronises `stream`. */
+lamb_status lamb_get_state(lamb_t h, int32_t which, float* dst, int32_t on_device, void* stream);
+
+/* Per tensor, from the last completed step (synchronises the device): ||w||^2 and ||u||^2
+ * (fp64, full tensor after the cross-shard combine) and the trust ratio.  Arrays have
+ * n_tensors entries; only tensors with a segment on this rank are written (others NaN).
+ * Any pointer may be NULL. */
+lamb_status lamb_get_tensor_stats(lamb_t h, double* w_sq, double* u_sq, float* ratio);
+
+/* Changes a group's learning rate for subsequent steps (schedules live outside, Z13). */
+lamb_status lamb_set_lr(lamb_t h, int32_t group, float lr);
+
+/* ---------------- measurement (CUDA events, §5.1 P:21-35 style) ---------------- */
+#define LAMB_PH_BARRIER_IN 0   /* cross-GPU "grads ready" barrier (FUSED, D > 1) */
+#define LAMB_PH_PASS_A 1       /* a1+a2: (fused RS) + moments + update + partial norms */
+#define LAMB_PH_FINALIZE 2     /* a3+a4: segment sums, local trust ratios */
+#define LAMB_PH_EXCHANGE 3     /* a3 cross-shard combine of straddlers + their ratios */
+#define LAMB_PH_PASS_B 4       /* a5+a6: apply + bf16 cast (+ fused AG stores) */
+#define LAMB_PH_BARRIER_OUT 5  /* cross-GPU "params complete" barrier */
+#define LAMB_N_PHASES 6
+/* Needs LAMB_FLAG_TIMING.  Starts recording the next `max_steps` steps. */
+lamb_status lamb_timing_begin(lamb_t h, int32_t max_steps);
+/* Synchronises and writes ms[n][LAMB_N_PHASES] for the n recorded steps; *n_steps = n. */
+lamb_status lamb_timing_read(lamb_t h, float* ms, int32_t* n_steps);
+/* Number of kernels this handle has launched (all steps so far). */
+int64_t lamb_launch_count(lamb_t h);
+
+const char* lamb_last_error(lamb_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAMB_H_ */

@@ -1,0 +1,834 @@
+// lamb_api.cu — implementation of include/lamb.h and include/lamb_synth.h.
+//
+// lamb_create: planner (row a0) -> work items -> device buffers -> NCCL communicator ->
+// (FUSED) CUDA-IPC mapping of every peer's grad / param / sync buffers over NVLink.
+// lamb_step (rows a1-a7), FUSED mode, all on the caller's stream:
+//     barrier("grads ready") -> pass A (peer bf16 loads, fp32 sum = fused reduce-scatter)
+//     -> finalize segments (+ straddler rows stored into every peer) -> barrier
+//     -> finalize straddlers -> pass B (bf16 params stored into every peer = fused
+//     all-gather) -> barrier("params complete").
+// NCCL mode (baseline): per bucket upcast + ncclReduceScatter(fp32) on a comm stream,
+// overlapped with pass A of earlier buckets; ncclAllGather(fp64) of straddler rows;
+// per-bucket ncclAllGather(bf16) of params overlapped with pass B of later buckets.
+// D = 1: pass A -> finalize -> pass B.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/lamb.h"
+#include "../../include/lamb_synth.h"
+#include "lamb_kernels.cuh"
+#include "planner.hpp"
+#include "synth.cuh"
+
+using namespace lamb;
+
+static thread_local std::string g_last_error;
+
+struct lamb_plan_ctx {
+    Plan plan;
+};
+
+struct lamb_ctx {
+    Plan plan;
+    lamb_config cfg{};
+    std::vector<lamb_group> groups;
+    std::string err;
+    int device = 0;
+    bool master_set = false;
+    int64_t launches = 0;
+    // device buffers (own)
+    __nv_bfloat16* grad = nullptr;     // flat
+    __nv_bfloat16* param = nullptr;    // flat
+    float *w = nullptr, *m = nullptr, *v = nullptr;   // shard
+    Item* items = nullptr;
+    int64_t n_items = 0;
+    std::vector<int64_t> bucket_item_begin;   // [B+1] items of bucket b: [b], [b+1)
+    double2* partials = nullptr;
+    SegDesc* segs = nullptr;
+    float* scale = nullptr;
+    double *w_sq = nullptr, *u_sq = nullptr;
+    float* ratio = nullptr;
+    int32_t *strad_slots = nullptr, *strad_tensor = nullptr, *strad_group = nullptr;
+    int32_t n_local_strad = 0;
+    // sync buffer: [flags uint64 x 8][epoch uint64][pad][xbuf double2 x D x n_strad]
+    char* sync = nullptr;
+    size_t sync_bytes = 0;
+    int* err_flag_host = nullptr;   // host-mapped
+    int* err_flag_dev = nullptr;
+    // peers (FUSED): index j = rank j (own entry = own pointer)
+    __nv_bfloat16* peer_grad[LAMB_MAX_RANKS] = {};
+    __nv_bfloat16* peer_param[LAMB_MAX_RANKS] = {};
+    char* peer_sync[LAMB_MAX_RANKS] = {};
+    // NCCL
+    ncclComm_t comm = nullptr;
+    cudaStream_t comm_stream = nullptr;
+    float* g32 = nullptr;          // NCCL mode: reduced fp32 grad shard
+    float* up32[2] = {nullptr, nullptr};   // NCCL mode: upcast staging, 2 buckets
+    int64_t max_bucket = 0;
+    std::vector<cudaEvent_t> ev_rs, ev_a, ev_b, ev_up;
+    cudaEvent_t ev_start = nullptr, ev_x = nullptr, ev_done = nullptr;
+    int grid_a = 0, grid_b = 0;
+    // synth tables (device)
+    int64_t *d_tensor_off = nullptr, *d_numel = nullptr, *d_shard_base = nullptr,
+            *d_bucket_base = nullptr, *d_bucket_slice = nullptr;
+    // timing
+    std::vector<cudaEvent_t> tev;   // [max_steps][LAMB_N_PHASES + 1]
+    int32_t t_max = 0, t_n = 0;
+
+    uint64_t* flags(int j) const { return reinterpret_cast<uint64_t*>(peer_sync[j]); }
+    uint64_t* epoch() const { return reinterpret_cast<uint64_t*>(sync + 8 * LAMB_MAX_RANKS); }
+    double2* xbuf(int j) const {
+        return reinterpret_cast<double2*>((j < 0 ? sync : peer_sync[j]) + 128);
+    }
+};
+
+// ------------------------------------------------------------------ error plumbing
+static lamb_status fail(lamb_ctx* h, lamb_status st, const std::string& msg) {
+    g_last_error = msg;
+    if (h) h->err = msg;
+    return st;
+}
+#define CUDA_TRY(h, call)                                                                     \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(h, e_ == cudaErrorMemoryAllocation ? LAMB_ENOMEM : LAMB_ECUDA,        \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+    } while (0)
+#define NCCL_TRY(h, call)                                                                     \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail(h, LAMB_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));   \
+    } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t n) {
+    *p = nullptr;
+    if (n == 0) n = 1;
+    return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+}
+
+template <typename T>
+static cudaError_t upload(T** p, const std::vector<T>& v) {
+    cudaError_t e = dalloc(p, v.size());
+    if (e != cudaSuccess) return e;
+    if (v.empty()) return cudaSuccess;
+    return cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+// ------------------------------------------------------------------ planner ABI
+extern "C" lamb_status lamb_plan_create(const lamb_tensor* tensors, int64_t n_tensors,
+                                        int32_t world_size, int32_t rank, int64_t cap,
+                                        lamb_plan_t* out) {
+    if (!out || !tensors || n_tensors < 1) return fail(nullptr, LAMB_EINVAL, "bad arguments");
+    std::vector<int64_t> numel(n_tensors);
+    std::vector<int32_t> grp(n_tensors);
+    for (int64_t i = 0; i < n_tensors; ++i) {
+        numel[i] = tensors[i].numel;
+        grp[i] = tensors[i].group;
+    }
+    auto* p = new lamb_plan_ctx();
+    std::string why = build_plan(numel.data(), grp.data(), n_tensors, world_size, rank, cap, &p->plan);
+    if (!why.empty()) {
+        delete p;
+        return fail(nullptr, LAMB_EINVAL, why);
+    }
+    *out = p;
+    return LAMB_OK;
+}
+
+static void fill_view(const Plan& p, lamb_plan_view* v) {
+    v->n_tensors = p.n_tensors();
+    v->n_buckets = p.n_buckets();
+    v->n_segments = p.n_segments();
+    v->n_straddlers = (int64_t)p.straddlers.size();
+    v->flat_size = p.flat_size;
+    v->shard_size = p.shard_size;
+    v->world_size = p.world;
+    v->rank = p.rank;
+    v->tensor_off = p.tensor_off.data();
+    v->tensor_bucket = p.tensor_bucket.data();
+    v->buckets = p.buckets.data();
+    v->segments = p.segments.data();
+    v->straddlers = p.straddlers.data();
+}
+
+extern "C" lamb_status lamb_plan_get(lamb_plan_t plan, lamb_plan_view* out) {
+    if (!plan || !out) return fail(nullptr, LAMB_EINVAL, "null argument");
+    fill_view(plan->plan, out);
+    return LAMB_OK;
+}
+
+extern "C" void lamb_plan_destroy(lamb_plan_t plan) { delete plan; }
+
+// ------------------------------------------------------------------ lifecycle
+extern "C" lamb_status lamb_get_unique_id(uint8_t id[LAMB_UNIQUE_ID_BYTES]) {
+    if (!id) return fail(nullptr, LAMB_EINVAL, "null id");
+    static_assert(sizeof(ncclUniqueId) == LAMB_UNIQUE_ID_BYTES, "nccl id size");
+    ncclUniqueId u;
+    ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) return fail(nullptr, LAMB_ENCCL, ncclGetErrorString(r));
+    memcpy(id, &u, sizeof(u));
+    return LAMB_OK;
+}
+
+static std::string check_group(const lamb_group& g) {
+    if (!(g.lr >= 0.f)) return "lr must be >= 0";
+    if (!(g.beta1 >= 0.f && g.beta1 < 1.f)) return "beta1 must be in [0,1)";
+    if (!(g.beta2 >= 0.f && g.beta2 < 1.f)) return "beta2 must be in [0,1)";
+    if (!(g.eps >= 0.f)) return "eps must be >= 0";
+    if (!(g.weight_decay >= 0.f)) return "weight_decay must be >= 0";
+    if (g.adapt != 0 && g.adapt != 1) return "adapt must be 0 or 1";
+    if (g.bias_correction != 0 && g.bias_correction != 1) return "bias_correction must be 0 or 1";
+    return std::string();
+}
+
+static void free_ctx(lamb_ctx* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    for (int j = 0; j < h->cfg.world_size && j < LAMB_MAX_RANKS; ++j) {
+        if (j == h->cfg.rank) continue;
+        if (h->peer_grad[j]) cudaIpcCloseMemHandle(h->peer_grad[j]);
+        if (h->peer_param[j]) cudaIpcCloseMemHandle(h->peer_param[j]);
+        if (h->peer_sync[j]) cudaIpcCloseMemHandle(h->peer_sync[j]);
+    }
+    void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->partials, h->segs, h->scale,
+                    h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
+                    h->sync, h->g32, h->up32[0], h->up32[1], h->d_tensor_off, h->d_numel,
+                    h->d_shard_base, h->d_bucket_base, h->d_bucket_slice};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h->err_flag_host) cudaFreeHost(h->err_flag_host);
+    for (auto* vec : {&h->ev_rs, &h->ev_a, &h->ev_b, &h->ev_up, &h->tev})
+        for (cudaEvent_t e : *vec) cudaEventDestroy(e);
+    for (cudaEvent_t e : {h->ev_start, h->ev_x, h->ev_done})
+        if (e) cudaEventDestroy(e);
+    if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    if (h->comm) ncclCommDestroy(h->comm);
+    delete h;
+}
+
+static lamb_status build_tables(lamb_ctx* h) {
+    const Plan& p = h->plan;
+    const int64_t nseg = p.n_segments();
+    std::vector<Item> items;
+    std::vector<SegDesc> segs(nseg);
+    std::vector<int64_t> strad_slot_of(p.n_tensors(), -1);
+    for (size_t k = 0; k < p.straddlers.size(); ++k) strad_slot_of[p.straddlers[k]] = (int64_t)k;
+    std::vector<int32_t> ls_slot, ls_tensor, ls_group;
+    const int64_t B = p.n_buckets();
+    h->bucket_item_begin.assign(B + 1, 0);
+    int64_t b = 0;
+    for (int64_t s = 0; s < nseg; ++s) {
+        const int64_t t = p.segments[4 * s], soff = p.segments[4 * s + 1];
+        const int64_t len = p.segments[4 * s + 3];
+        const int64_t tb = p.tensor_bucket[t];
+        while (b < tb) h->bucket_item_begin[++b] = (int64_t)items.size();
+        const int64_t slice = p.buckets[4 * tb + 1] / p.world;
+        const int64_t flat0 = p.buckets[4 * tb] + (int64_t)p.rank * slice + (soff - p.shard_base[tb]);
+        // the segment rounded up to 8 stays inside zero padding (P2: next start is 8-aligned,
+        // P6: slice ends are 128-aligned)
+        const int64_t len8 = (len + 7) / 8 * 8;
+        segs[s].item_begin = (int64_t)items.size();
+        for (int64_t o = 0; o < len8; o += kItemElems) {
+            const int64_t n = std::min<int64_t>(kItemElems, len8 - o);
+            Item it;
+            it.shard_off = soff + o;
+            it.flat_off = flat0 + o;
+            it.n_chunk = (int32_t)(n / kChunk);
+            it.tensor = (int32_t)t;
+            it.group = p.group[t];
+            it.seg = (int32_t)s;
+            items.push_back(it);
+        }
+        segs[s].item_end = (int64_t)items.size();
+        segs[s].tensor = (int32_t)t;
+        segs[s].group = p.group[t];
+        segs[s].strad_slot = (int32_t)strad_slot_of[t];
+        segs[s].pad = 0;
+        if (strad_slot_of[t] >= 0) {
+            ls_slot.push_back((int32_t)strad_slot_of[t]);
+            ls_tensor.push_back((int32_t)t);
+            ls_group.push_back(p.group[t]);
+        }
+    }
+    while (b < B) h->bucket_item_begin[++b] = (int64_t)items.size();
+    h->n_items = (int64_t)items.size();
+    h->n_local_strad = (int32_t)ls_slot.size();
+    CUDA_TRY(h, upload(&h->items, items));
+    CUDA_TRY(h, upload(&h->segs, segs));
+    CUDA_TRY(h, upload(&h->strad_slots, ls_slot));
+    CUDA_TRY(h, upload(&h->strad_tensor, ls_tensor));
+    CUDA_TRY(h, upload(&h->strad_group, ls_group));
+    CUDA_TRY(h, dalloc(&h->partials, (size_t)h->n_items));
+    const size_t T = (size_t)p.n_tensors();
+    CUDA_TRY(h, dalloc(&h->scale, T));
+    CUDA_TRY(h, dalloc(&h->w_sq, T));
+    CUDA_TRY(h, dalloc(&h->u_sq, T));
+    CUDA_TRY(h, dalloc(&h->ratio, T));
+    CUDA_TRY(h, cudaMemset(h->w_sq, 0xFF, T * sizeof(double)));   // NaN = not touched
+    CUDA_TRY(h, cudaMemset(h->u_sq, 0xFF, T * sizeof(double)));
+    CUDA_TRY(h, cudaMemset(h->ratio, 0xFF, T * sizeof(float)));
+    // synth tables
+    std::vector<int64_t> bb(B), bs(B);
+    for (int64_t k = 0; k < B; ++k) {
+        bb[k] = p.buckets[4 * k];
+        bs[k] = p.buckets[4 * k + 1] / p.world;
+        h->max_bucket = std::max(h->max_bucket, p.buckets[4 * k + 1]);
+    }
+    CUDA_TRY(h, upload(&h->d_tensor_off, p.tensor_off));
+    CUDA_TRY(h, upload(&h->d_numel, p.numel));
+    CUDA_TRY(h, upload(&h->d_shard_base, p.shard_base));
+    CUDA_TRY(h, upload(&h->d_bucket_base, bb));
+    CUDA_TRY(h, upload(&h->d_bucket_slice, bs));
+    return LAMB_OK;
+}
+
+static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
+    const int D = h->cfg.world_size, r = h->cfg.rank;
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof(u));
+    NCCL_TRY(h, ncclCommInitRank(&h->comm, D, u, r));
+    for (int j = 0; j < D; ++j) {
+        h->peer_grad[j] = h->grad;
+        h->peer_param[j] = h->param;
+        h->peer_sync[j] = h->sync;
+    }
+    if (h->cfg.comm_mode != LAMB_COMM_FUSED) return LAMB_OK;
+    // exchange IPC handles of grad / param / sync through NCCL (one all-gather)
+    cudaIpcMemHandle_t mine[3];
+    CUDA_TRY(h, cudaIpcGetMemHandle(&mine[0], h->grad));
+    CUDA_TRY(h, cudaIpcGetMemHandle(&mine[1], h->param));
+    CUDA_TRY(h, cudaIpcGetMemHandle(&mine[2], h->sync));
+    const size_t hb = sizeof(mine);
+    char* dbuf = nullptr;
+    CUDA_TRY(h, cudaMalloc(&dbuf, hb * (D + 1)));
+    CUDA_TRY(h, cudaMemcpy(dbuf + hb * D, mine, hb, cudaMemcpyHostToDevice));
+    NCCL_TRY(h, ncclAllGather(dbuf + hb * D, dbuf, hb, ncclChar, h->comm, 0));
+    std::vector<cudaIpcMemHandle_t> all(3 * D);
+    CUDA_TRY(h, cudaMemcpy(all.data(), dbuf, hb * D, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    for (int j = 0; j < D; ++j) {
+        if (j == r) continue;
+        void* p = nullptr;
+        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[3 * j + 0], cudaIpcMemLazyEnablePeerAccess));
+        h->peer_grad[j] = static_cast<__nv_bfloat16*>(p);
+        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[3 * j + 1], cudaIpcMemLazyEnablePeerAccess));
+        h->peer_param[j] = static_cast<__nv_bfloat16*>(p);
+        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[3 * j + 2], cudaIpcMemLazyEnablePeerAccess));
+        h->peer_sync[j] = static_cast<char*>(p);
+    }
+    // make sure every rank has mapped everything before the first step
+    int* one = nullptr;
+    CUDA_TRY(h, cudaMalloc(&one, sizeof(int)));
+    NCCL_TRY(h, ncclAllReduce(one, one, 1, ncclInt, ncclSum, h->comm, 0));
+    CUDA_TRY(h, cudaDeviceSynchronize());
+    cudaFree(one);
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors,
+                                   const lamb_group* groups, int32_t n_groups,
+                                   const lamb_config* cfg, const uint8_t* id, lamb_t* out) {
+    if (!out || !tensors || !groups || !cfg) return fail(nullptr, LAMB_EINVAL, "null argument");
+    *out = nullptr;
+    if (n_groups < 1 || n_groups > LAMB_MAX_GROUPS)
+        return fail(nullptr, LAMB_EINVAL, "n_groups must be in [1, 64]");
+    for (int32_t k = 0; k < n_groups; ++k) {
+        std::string why = check_group(groups[k]);
+        if (!why.empty()) return fail(nullptr, LAMB_EINVAL, "group " + std::to_string(k) + ": " + why);
+    }
+    if (n_tensors < 1) return fail(nullptr, LAMB_EINVAL, "n_tensors must be >= 1");
+    for (int64_t i = 0; i < n_tensors; ++i) {
+        if (tensors[i].group < 0 || tensors[i].group >= n_groups)
+            return fail(nullptr, LAMB_EINVAL, "tensor " + std::to_string(i) + ": group out of range");
+        if (tensors[i].reserved != 0) return fail(nullptr, LAMB_EINVAL, "reserved must be 0");
+    }
+    if (cfg->world_size > 1 && !id) return fail(nullptr, LAMB_EINVAL, "unique id required for D > 1");
+    if (cfg->world_size > 1 && cfg->comm_mode != LAMB_COMM_NCCL && cfg->comm_mode != LAMB_COMM_FUSED)
+        return fail(nullptr, LAMB_EUNSUPPORTED, "comm_mode not supported in ABI v1");
+    if (!(cfg->grad_scale >= 0.f)) return fail(nullptr, LAMB_EINVAL, "grad_scale must be >= 0");
+
+    auto* h = new lamb_ctx();
+    h->cfg = *cfg;
+    h->device = cfg->device;
+    h->groups.assign(groups, groups + n_groups);
+    if (h->cfg.grad_scale == 0.f) h->cfg.grad_scale = 1.0f / (float)cfg->world_size;
+    std::vector<int64_t> numel(n_tensors);
+    std::vector<int32_t> grp(n_tensors);
+    for (int64_t i = 0; i < n_tensors; ++i) {
+        numel[i] = tensors[i].numel;
+        grp[i] = tensors[i].group;
+    }
+    std::string why = build_plan(numel.data(), grp.data(), n_tensors, cfg->world_size, cfg->rank,
+                                 cfg->bucket_cap_elems, &h->plan);
+    if (!why.empty()) {
+        fail(nullptr, LAMB_EINVAL, why);
+        delete h;
+        return LAMB_EINVAL;
+    }
+    lamb_status st = LAMB_OK;
+    auto bail = [&](lamb_status s) {
+        g_last_error = h->err;
+        free_ctx(h);
+        return s;
+    };
+    cudaError_t ce = cudaSetDevice(cfg->device);
+    if (ce != cudaSuccess) {
+        fail(h, LAMB_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(ce));
+        return bail(LAMB_ECUDA);
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10 || prop.minor != 0) {
+        fail(h, LAMB_EUNSUPPORTED, "device is not sm_100 (B200); no fallback path exists");
+        return bail(LAMB_EUNSUPPORTED);
+    }
+#define STEP(x)                      \
+    do {                             \
+        st = (x);                    \
+        if (st != LAMB_OK) return bail(st); \
+    } while (0)
+#define CUDA_STEP(x)                                                                         \
+    do {                                                                                     \
+        cudaError_t e_ = (x);                                                                \
+        if (e_ != cudaSuccess) {                                                             \
+            st = fail(h, e_ == cudaErrorMemoryAllocation ? LAMB_ENOMEM : LAMB_ECUDA,         \
+                      std::string(#x) + ": " + cudaGetErrorString(e_));                      \
+            return bail(st);                                                                 \
+        }                                                                                    \
+    } while (0)
+    const Plan& p = h->plan;
+    const int D = cfg->world_size;
+    CUDA_STEP(dalloc(&h->grad, (size_t)p.flat_size));
+    CUDA_STEP(dalloc(&h->param, (size_t)p.flat_size));
+    CUDA_STEP(cudaMemset(h->grad, 0, (size_t)p.flat_size * 2));
+    CUDA_STEP(cudaMemset(h->param, 0, (size_t)p.flat_size * 2));
+    CUDA_STEP(dalloc(&h->w, (size_t)p.shard_size));
+    CUDA_STEP(dalloc(&h->m, (size_t)p.shard_size));
+    CUDA_STEP(dalloc(&h->v, (size_t)p.shard_size));
+    CUDA_STEP(cudaMemset(h->w, 0, (size_t)p.shard_size * 4));
+    CUDA_STEP(cudaMemset(h->m, 0, (size_t)p.shard_size * 4));
+    CUDA_STEP(cudaMemset(h->v, 0, (size_t)p.shard_size * 4));
+    STEP(build_tables(h));
+    h->sync_bytes = 128 + sizeof(double2) * (size_t)D * std::max<size_t>(1, p.straddlers.size());
+    CUDA_STEP(dalloc(&h->sync, h->sync_bytes));
+    CUDA_STEP(cudaMemset(h->sync, 0, h->sync_bytes));
+    CUDA_STEP(cudaHostAlloc(&h->err_flag_host, sizeof(int), cudaHostAllocMapped));
+    *h->err_flag_host = 0;
+    CUDA_STEP(cudaHostGetDevicePointer(&h->err_flag_dev, h->err_flag_host, 0));
+    h->grid_a = pass_grid(cfg->device, D, false, false, 1);
+    h->grid_b = pass_grid(cfg->device, 1, false, true, D);
+    CUDA_STEP(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
+    CUDA_STEP(cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming));
+    CUDA_STEP(cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming));
+    for (int j = 0; j < LAMB_MAX_RANKS; ++j) {
+        h->peer_grad[j] = h->grad;
+        h->peer_param[j] = h->param;
+        h->peer_sync[j] = h->sync;
+    }
+    if (D > 1) {
+        STEP(setup_comm(h, id));
+        if (cfg->comm_mode == LAMB_COMM_NCCL) {
+            CUDA_STEP(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+            CUDA_STEP(dalloc(&h->g32, (size_t)p.shard_size));
+            CUDA_STEP(cudaMemset(h->g32, 0, (size_t)p.shard_size * 4));
+            CUDA_STEP(dalloc(&h->up32[0], (size_t)h->max_bucket));
+            CUDA_STEP(dalloc(&h->up32[1], (size_t)h->max_bucket));
+            const int64_t B = p.n_buckets();
+            for (auto* vec : {&h->ev_rs, &h->ev_a, &h->ev_b, &h->ev_up}) {
+                vec->resize(B);
+                for (auto& e : *vec) CUDA_STEP(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+        }
+    }
+    CUDA_STEP(cudaDeviceSynchronize());
+    *out = h;
+    return LAMB_OK;
+#undef STEP
+#undef CUDA_STEP
+}
+
+extern "C" void lamb_destroy(lamb_t h) { free_ctx(h); }
+
+// ------------------------------------------------------------------ the step
+static void group_consts(const lamb_ctx* h, int64_t t, GroupConst* out) {
+    for (size_t k = 0; k < h->groups.size(); ++k) {
+        const lamb_group& g = h->groups[k];
+        GroupConst& c = out[k];
+        c.lr = g.lr;
+        c.b1 = g.beta1;
+        c.b2 = g.beta2;
+        c.omb1 = (float)(1.0 - (double)g.beta1);   // exact for fp32 betas in [0.5, 1)
+        c.omb2 = (float)(1.0 - (double)g.beta2);
+        c.eps = g.eps;
+        c.wd = g.weight_decay;
+        // bias correction in double on the host (reading Z14), passed as fp32
+        c.c1 = g.bias_correction ? (float)(1.0 / (1.0 - std::pow((double)g.beta1, (double)t))) : 1.0f;
+        c.c2 = g.bias_correction ? (float)(1.0 / (1.0 - std::pow((double)g.beta2, (double)t))) : 1.0f;
+        c.adapt = g.adapt;
+    }
+}
+
+static inline void mark(lamb_ctx* h, int phase, cudaStream_t s) {
+    if (h->t_n < h->t_max) cudaEventRecord(h->tev[(size_t)h->t_n * (LAMB_N_PHASES + 1) + phase], s);
+}
+
+#define LAUNCH(h, call)                                                                       \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) return fail(h, LAMB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+        ++(h)->launches;                                                                      \
+    } while (0)
+
+static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStream_t s) {
+    const Plan& p = h->plan;
+    const int D = h->cfg.world_size, r = h->cfg.rank;
+    const bool fused = D > 1 && h->cfg.comm_mode == LAMB_COMM_FUSED;
+    const bool nccl = D > 1 && h->cfg.comm_mode == LAMB_COMM_NCCL;
+
+    StepParams sp;
+    memset(&sp, 0, sizeof(sp));
+    sp.items = h->items;
+    sp.item_begin = 0;
+    sp.item_end = h->n_items;
+    sp.grad_scale = h->cfg.grad_scale;
+    sp.w = h->w;
+    sp.m = h->m;
+    sp.v = h->v;
+    sp.partials = h->partials;
+    sp.scale = h->scale;
+    group_consts(h, t, sp.groups);
+    FinalizeParams fp;
+    memset(&fp, 0, sizeof(fp));
+    fp.segs = h->segs;
+    fp.n_segs = p.n_segments();
+    fp.partials = h->partials;
+    fp.scale = h->scale;
+    fp.w_sq = h->w_sq;
+    fp.u_sq = h->u_sq;
+    fp.ratio = h->ratio;
+    fp.world = D;
+    fp.rank = r;
+    fp.n_strad = (int32_t)p.straddlers.size();
+    fp.strad_slots = h->strad_slots;
+    fp.strad_tensor = h->strad_tensor;
+    fp.strad_group = h->strad_group;
+    fp.n_local_strad = h->n_local_strad;
+    fp.xbuf = h->xbuf(-1);
+    memcpy(fp.groups, sp.groups, sizeof(sp.groups));
+
+    mark(h, 0, s);
+    if (!nccl) {
+        // ---------------- D = 1 or FUSED
+        uint64_t* flags[LAMB_MAX_RANKS];
+        for (int j = 0; j < D; ++j) flags[j] = h->flags(j);
+        if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+        mark(h, 1, s);
+        for (int j = 0; j < D; ++j)
+            sp.gsrc[j] = fused ? h->peer_grad[j] : (grads ? (const __nv_bfloat16*)grads : h->grad);
+        LAUNCH(h, launch_pass_a(sp, D, false, h->grid_a, s));
+        mark(h, 2, s);
+        for (int j = 0; j < D; ++j) fp.xrow[j] = h->xbuf(fused ? j : -1);
+        LAUNCH(h, launch_finalize_segments(fp, s));
+        mark(h, 3, s);
+        if (fused) {
+            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+            if (h->n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
+        }
+        mark(h, 4, s);
+        for (int j = 0; j < D; ++j) sp.pdst[j] = fused ? h->peer_param[j] : h->param;
+        LAUNCH(h, launch_pass_b(sp, fused ? D : 1, h->grid_b, s));
+        mark(h, 5, s);
+        if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+        mark(h, 6, s);
+        return LAMB_OK;
+    }
+
+    // ---------------- NCCL baseline, per-bucket pipeline on (s, comm_stream)
+    const int64_t B = p.n_buckets();
+    const __nv_bfloat16* gsrc = grads ? (const __nv_bfloat16*)grads : h->grad;
+    CUDA_TRY(h, cudaEventRecord(h->ev_start, s));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_start, 0));
+    mark(h, 1, s);
+    sp.g32 = h->g32;
+    for (int64_t b = 0; b < B; ++b) {
+        const int64_t base = p.buckets[4 * b], S = p.buckets[4 * b + 1];
+        float* up = h->up32[b & 1];
+        // staging buffer b&1 is free once pass A of bucket b-2 ... the RS of bucket b-2 is done
+        // (the RS reads `up`), which comm_stream order already guarantees.
+        LAUNCH(h, launch_upcast_bf16(gsrc + base, up, S, h->comm_stream));
+        NCCL_TRY(h, ncclReduceScatter(up, h->g32 + p.shard_base[b], (size_t)(S / D), ncclFloat,
+                                      ncclSum, h->comm, h->comm_stream));
+        CUDA_TRY(h, cudaEventRecord(h->ev_rs[b], h->comm_stream));
+    }
+    for (int64_t b = 0; b < B; ++b) {
+        CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_rs[b], 0));
+        sp.item_begin = h->bucket_item_begin[b];
+        sp.item_end = h->bucket_item_begin[b + 1];
+        LAUNCH(h, launch_pass_a(sp, 0, true, h->grid_a, s));
+    }
+    mark(h, 2, s);
+    for (int j = 0; j < D; ++j) fp.xrow[j] = h->xbuf(-1);
+    LAUNCH(h, launch_finalize_segments(fp, s));
+    mark(h, 3, s);
+    if (!p.straddlers.empty()) {
+        const size_t n = p.straddlers.size() * 2;
+        double* xb = reinterpret_cast<double*>(h->xbuf(-1));
+        NCCL_TRY(h, ncclAllGather(xb + (size_t)r * n, xb, n, ncclDouble, h->comm, s));
+        if (h->n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
+    }
+    mark(h, 4, s);
+    sp.pdst[0] = h->param;
+    for (int64_t b = 0; b < B; ++b) {
+        sp.item_begin = h->bucket_item_begin[b];
+        sp.item_end = h->bucket_item_begin[b + 1];
+        LAUNCH(h, launch_pass_b(sp, 1, h->grid_b, s));
+        CUDA_TRY(h, cudaEventRecord(h->ev_b[b], s));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_b[b], 0));
+        const int64_t base = p.buckets[4 * b], sl = p.buckets[4 * b + 1] / D;
+        NCCL_TRY(h, ncclAllGather(h->param + base + (int64_t)r * sl, h->param + base, (size_t)sl,
+                                  ncclBfloat16, h->comm, h->comm_stream));
+    }
+    CUDA_TRY(h, cudaEventRecord(h->ev_done, h->comm_stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_done, 0));
+    mark(h, 5, s);
+    mark(h, 6, s);
+    return LAMB_OK;
+}
+
+static lamb_status check_async(lamb_ctx* h) {
+    if (h->err_flag_host && *(volatile int*)h->err_flag_host)
+        return fail(h, LAMB_ECUDA, "cross-GPU barrier timed out in an earlier step (peer missing)");
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return fail(h, LAMB_ECUDA, std::string("pending CUDA error: ") + cudaGetErrorString(e));
+    if (h->comm) {
+        ncclResult_t ae;
+        if (ncclCommGetAsyncError(h->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+            return fail(h, LAMB_ENCCL, std::string("NCCL async error: ") + ncclGetErrorString(ae));
+    }
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void* stream) {
+    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
+    if (step < 1) return fail(h, LAMB_EINVAL, "step must be >= 1");
+    if (grads && h->cfg.world_size > 1 && h->cfg.comm_mode == LAMB_COMM_FUSED)
+        return fail(h, LAMB_EINVAL, "external grads are not allowed in FUSED mode with D > 1");
+    if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step before lamb_set_master / lamb_synth_init");
+    lamb_status st = check_async(h);
+    if (st != LAMB_OK) return st;
+    cudaSetDevice(h->device);
+    st = step_impl(h, grads, step, static_cast<cudaStream_t>(stream));
+    if (h->t_n < h->t_max) ++h->t_n;
+    return st;
+}
+
+extern "C" lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_params,
+                                      int64_t step, void* stream) {
+    if (!h || !host_grads || !host_params) return fail(h, LAMB_EINVAL, "null argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaSetDevice(h->device);
+    const size_t bytes = (size_t)h->plan.flat_size * 2;
+    CUDA_TRY(h, cudaMemcpyAsync(h->grad, host_grads, bytes, cudaMemcpyHostToDevice, s));
+    lamb_status st = lamb_step(h, nullptr, step, stream);
+    if (st != LAMB_OK) return st;
+    CUDA_TRY(h, cudaMemcpyAsync(host_params, h->param, bytes, cudaMemcpyDeviceToHost, s));
+    return LAMB_OK;
+}
+
+// ------------------------------------------------------------------ queries / state
+extern "C" lamb_status lamb_query_plan(lamb_t h, lamb_plan_view* out) {
+    if (!h || !out) return fail(h, LAMB_EINVAL, "null argument");
+    fill_view(h->plan, out);
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_buffer(lamb_t h, int32_t which, void** dev_ptr, int64_t* n) {
+    if (!h || !dev_ptr || !n) return fail(h, LAMB_EINVAL, "null argument");
+    switch (which) {
+        case LAMB_BUF_GRAD: *dev_ptr = h->grad; *n = h->plan.flat_size; return LAMB_OK;
+        case LAMB_BUF_PARAM: *dev_ptr = h->param; *n = h->plan.flat_size; return LAMB_OK;
+        case LAMB_BUF_W: *dev_ptr = h->w; *n = h->plan.shard_size; return LAMB_OK;
+        case LAMB_BUF_M: *dev_ptr = h->m; *n = h->plan.shard_size; return LAMB_OK;
+        case LAMB_BUF_V: *dev_ptr = h->v; *n = h->plan.shard_size; return LAMB_OK;
+    }
+    return fail(h, LAMB_EINVAL, "unknown buffer");
+}
+
+extern "C" lamb_status lamb_set_master(lamb_t h, const float* full, int32_t on_device, void* stream) {
+    if (!h || !full) return fail(h, LAMB_EINVAL, "null argument");
+    cudaSetDevice(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Plan& p = h->plan;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (int64_t b = 0; b < p.n_buckets(); ++b) {
+        const int64_t sl = p.buckets[4 * b + 1] / p.world;
+        CUDA_TRY(h, cudaMemcpyAsync(h->w + p.shard_base[b], full + p.buckets[4 * b] + (int64_t)p.rank * sl,
+                                    (size_t)sl * 4, kind, s));
+    }
+    const float* src = full;
+    float* tmp = nullptr;
+    if (!on_device) {
+        CUDA_TRY(h, dalloc(&tmp, (size_t)p.flat_size));
+        CUDA_TRY(h, cudaMemcpyAsync(tmp, full, (size_t)p.flat_size * 4, cudaMemcpyHostToDevice, s));
+        src = tmp;
+    }
+    LAUNCH(h, launch_cast_to_bf16(src, h->param, p.flat_size, s));
+    CUDA_TRY(h, cudaMemsetAsync(h->m, 0, (size_t)p.shard_size * 4, s));
+    CUDA_TRY(h, cudaMemsetAsync(h->v, 0, (size_t)p.shard_size * 4, s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    if (tmp) cudaFree(tmp);
+    h->master_set = true;
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_get_state(lamb_t h, int32_t which, float* dst, int32_t on_device, void* stream) {
+    if (!h || !dst) return fail(h, LAMB_EINVAL, "null argument");
+    const float* src = which == LAMB_BUF_W ? h->w : which == LAMB_BUF_M ? h->m : which == LAMB_BUF_V ? h->v : nullptr;
+    if (!src) return fail(h, LAMB_EINVAL, "which must be LAMB_BUF_W/M/V");
+    cudaSetDevice(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(h, cudaMemcpyAsync(dst, src, (size_t)h->plan.shard_size * 4,
+                                on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_get_tensor_stats(lamb_t h, double* w_sq, double* u_sq, float* ratio) {
+    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
+    cudaSetDevice(h->device);
+    CUDA_TRY(h, cudaDeviceSynchronize());
+    const size_t T = (size_t)h->plan.n_tensors();
+    if (w_sq) CUDA_TRY(h, cudaMemcpy(w_sq, h->w_sq, T * 8, cudaMemcpyDeviceToHost));
+    if (u_sq) CUDA_TRY(h, cudaMemcpy(u_sq, h->u_sq, T * 8, cudaMemcpyDeviceToHost));
+    if (ratio) CUDA_TRY(h, cudaMemcpy(ratio, h->ratio, T * 4, cudaMemcpyDeviceToHost));
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_set_lr(lamb_t h, int32_t group, float lr) {
+    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
+    if (group < 0 || group >= (int32_t)h->groups.size()) return fail(h, LAMB_EINVAL, "group out of range");
+    if (!(lr >= 0.f)) return fail(h, LAMB_EINVAL, "lr must be >= 0");
+    h->groups[group].lr = lr;
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_timing_begin(lamb_t h, int32_t max_steps) {
+    if (!h || max_steps < 0) return fail(h, LAMB_EINVAL, "bad argument");
+    if (!(h->cfg.flags & LAMB_FLAG_TIMING)) return fail(h, LAMB_ESTATE, "handle created without LAMB_FLAG_TIMING");
+    cudaSetDevice(h->device);
+    CUDA_TRY(h, cudaDeviceSynchronize());
+    for (cudaEvent_t e : h->tev) cudaEventDestroy(e);
+    h->tev.assign((size_t)max_steps * (LAMB_N_PHASES + 1), nullptr);
+    for (auto& e : h->tev) CUDA_TRY(h, cudaEventCreate(&e));
+    h->t_max = max_steps;
+    h->t_n = 0;
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_timing_read(lamb_t h, float* ms, int32_t* n_steps) {
+    if (!h || !n_steps) return fail(h, LAMB_EINVAL, "null argument");
+    cudaSetDevice(h->device);
+    *n_steps = h->t_n;
+    for (int32_t k = 0; k < h->t_n; ++k) {
+        CUDA_TRY(h, cudaEventSynchronize(h->tev[(size_t)k * (LAMB_N_PHASES + 1) + LAMB_N_PHASES]));
+        for (int ph = 0; ph < LAMB_N_PHASES; ++ph) {
+            float x = 0.f;
+            CUDA_TRY(h, cudaEventElapsedTime(&x, h->tev[(size_t)k * (LAMB_N_PHASES + 1) + ph],
+                                             h->tev[(size_t)k * (LAMB_N_PHASES + 1) + ph + 1]));
+            if (ms) ms[(size_t)k * LAMB_N_PHASES + ph] = x;
+        }
+    }
+    return LAMB_OK;
+}
+
+extern "C" int64_t lamb_launch_count(lamb_t h) { return h ? h->launches : -1; }
+
+extern "C" const char* lamb_last_error(lamb_t h) {
+    return h ? h->err.c_str() : g_last_error.c_str();
+}
+
+// ------------------------------------------------------------------ synth ABI
+static lamb_status synth_tables(lamb_ctx* h, const lamb_synth_tensor* spec, SynthTables* t,
+                                int32_t** d_init, int32_t** d_gexp) {
+    const int64_t T = h->plan.n_tensors();
+    std::vector<int32_t> init(T), gexp(T);
+    for (int64_t i = 0; i < T; ++i) {
+        if (spec[i].init < 0 || spec[i].init > 2) return fail(h, LAMB_EINVAL, "bad init kind");
+        init[i] = spec[i].init;
+        gexp[i] = spec[i].gexp;
+    }
+    CUDA_TRY(h, upload(d_init, init));
+    CUDA_TRY(h, upload(d_gexp, gexp));
+    t->tensor_off = h->d_tensor_off;
+    t->numel = h->d_numel;
+    t->init = *d_init;
+    t->gexp = *d_gexp;
+    t->n_tensors = T;
+    t->shard_base = h->d_shard_base;
+    t->bucket_base = h->d_bucket_base;
+    t->bucket_slice = h->d_bucket_slice;
+    t->n_buckets = h->plan.n_buckets();
+    t->rank = h->plan.rank;
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_synth_init(lamb_t h, const lamb_synth_tensor* spec, uint64_t seed, void* stream) {
+    if (!h || !spec) return fail(h, LAMB_EINVAL, "null argument");
+    cudaSetDevice(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    SynthTables t;
+    int32_t *di = nullptr, *dg = nullptr;
+    lamb_status st = synth_tables(h, spec, &t, &di, &dg);
+    if (st == LAMB_OK) {
+        cudaError_t e = synth_init(t, seed, h->param, h->plan.flat_size, h->w, h->plan.shard_size, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(h->m, 0, (size_t)h->plan.shard_size * 4, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(h->v, 0, (size_t)h->plan.shard_size * 4, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = fail(h, LAMB_ECUDA, std::string("synth_init: ") + cudaGetErrorString(e));
+    }
+    if (di) cudaFree(di);
+    if (dg) cudaFree(dg);
+    if (st == LAMB_OK) h->master_set = true;
+    return st;
+}
+
+extern "C" lamb_status lamb_synth_grads(lamb_t h, const lamb_synth_tensor* spec, uint64_t seed,
+                                        uint32_t rank_term, uint32_t step, void* stream) {
+    if (!h || !spec) return fail(h, LAMB_EINVAL, "null argument");
+    cudaSetDevice(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    SynthTables t;
+    int32_t *di = nullptr, *dg = nullptr;
+    lamb_status st = synth_tables(h, spec, &t, &di, &dg);
+    if (st == LAMB_OK) {
+        cudaError_t e = synth_grads(t, seed, rank_term, step, reinterpret_cast<uint16_t*>(h->grad),
+                                    h->plan.flat_size, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = fail(h, LAMB_ECUDA, std::string("synth_grads: ") + cudaGetErrorString(e));
+    }
+    if (di) cudaFree(di);
+    if (dg) cudaFree(dg);
+    return st;
+}
+
+extern "C" lamb_status lamb_synth_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    if (!ctr || !key || !out) return fail(nullptr, LAMB_EINVAL, "null argument");
+    uint32_t in[6] = {ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1]};
+    uint32_t* d = nullptr;
+    CUDA_TRY(nullptr, cudaMalloc(&d, 10 * sizeof(uint32_t)));
+    CUDA_TRY(nullptr, cudaMemcpy(d, in, sizeof(in), cudaMemcpyHostToDevice));
+    CUDA_TRY(nullptr, synth_philox(d, d + 6));
+    CUDA_TRY(nullptr, cudaMemcpy(out, d + 6, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return LAMB_OK;
+}

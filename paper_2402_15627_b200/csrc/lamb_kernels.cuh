@@ -1,0 +1,95 @@
+// lamb_kernels.cuh — device-side data structures of the LAMB step (internal, not ABI).
+//
+// HBM layout: flat bf16 grad and param buffers in plan order (bucket after
+// bucket, 8-aligned tensors, zero padding); this rank's fp32 w, m, v shards in shard-local
+// order (its slice of bucket 0, then bucket 1, ...).  Work is cut into ITEMS: contiguous
+// pieces of ONE segment (tensor ∩ slice), <= kItemElems elements, 8-aligned starts.  One warp
+// owns one item at a time, so every per-item norm partial is an unsegmented, fixed-order
+// reduction (deterministic, no float atomics) — the "tensor-boundary table" of the north star
+// is the item -> segment -> tensor mapping.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "../../include/lamb.h"
+
+namespace lamb {
+
+constexpr int kThreads = 256;          // threads per CTA of the streaming passes
+constexpr int kChunk = 4;              // elements per lane access (16 B fp32, 8 B bf16)
+constexpr int64_t kItemElems = 4096;   // max elements per work item (multiple of 8)
+
+struct __align__(32) Item {
+    int64_t shard_off;   // first element in the fp32 shard (multiple of 8)
+    int64_t flat_off;    // same element in the flat bf16 buffers
+    int32_t n_chunk;     // ceil(len / 4) (len rounded up to 8: the tail is zero padding)
+    int32_t tensor;
+    int32_t group;
+    int32_t seg;
+};
+
+struct __align__(16) SegDesc {
+    int64_t item_begin, item_end;   // items of this segment (contiguous)
+    int32_t tensor, group;
+    int32_t strad_slot;             // index in the global straddler list, -1 if none
+    int32_t pad;
+};
+
+// Per-step constants of one group (host computes c1 = 1/(1-b1^t), c2 = 1/(1-b2^t) in double).
+struct GroupConst {
+    float lr, b1, omb1, b2, omb2, eps, wd, c1, c2;
+    int32_t adapt;
+};
+
+struct StepParams {
+    const Item* items;
+    int64_t item_begin, item_end;
+    // pass A gradient sources: flat bf16 grad buffers of ranks 0..nsrc-1 (peer-mapped), or
+    // g32 = this rank's fp32 reduced-gradient shard (NCCL mode)
+    const __nv_bfloat16* gsrc[LAMB_MAX_RANKS];
+    const float* g32;
+    float grad_scale;
+    float* w;
+    float* m;
+    float* v;
+    double2* partials;        // [n_items] (sum w^2, sum u^2)
+    const float* scale;       // [T] lr * ratio (pass B)
+    __nv_bfloat16* pdst[LAMB_MAX_RANKS];   // param buffers pass B stores into
+    GroupConst groups[LAMB_MAX_GROUPS];
+};
+
+struct FinalizeParams {
+    const SegDesc* segs;
+    int64_t n_segs;
+    const double2* partials;
+    float* scale;             // [T]
+    double* w_sq;             // [T] stats
+    double* u_sq;
+    float* ratio;
+    // straddler exchange: xrow[j] points at rank j's exchange buffer ([D][n_strad] double2);
+    // this rank writes its row (index `rank`) into every rank's buffer.
+    double2* xrow[LAMB_MAX_RANKS];
+    int32_t world, rank;
+    int32_t n_strad;
+    // straddler finalize: local slots this rank touches
+    const int32_t* strad_slots;     // [n_local_strad] slot index
+    const int32_t* strad_tensor;    // [n_local_strad]
+    const int32_t* strad_group;     // [n_local_strad]
+    int32_t n_local_strad;
+    const double2* xbuf;            // this rank's exchange buffer
+    GroupConst groups[LAMB_MAX_GROUPS];
+};
+
+// Host launchers (lamb_kernels.cu).  `occ_grid` = persistent grid size.
+cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int grid, cudaStream_t s);
+cudaError_t launch_pass_b(const StepParams& p, int ndst, int grid, cudaStream_t s);
+cudaError_t launch_finalize_segments(const FinalizeParams& p, cudaStream_t s);
+cudaError_t launch_finalize_straddlers(const FinalizeParams& p, cudaStream_t s);
+cudaError_t launch_barrier(uint64_t* const* flags, uint64_t* epoch, int rank, int world,
+                           int* err_flag, cudaStream_t s);
+cudaError_t launch_upcast_bf16(const __nv_bfloat16* src, float* dst, int64_t n, cudaStream_t s);
+cudaError_t launch_cast_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t s);
+int pass_grid(int device, int nsrc, bool g32, bool pass_b, int ndst);
+
+}  // namespace lamb

@@ -1,0 +1,86 @@
+"""CPU checks of the boundary: liblamb.so loads without a GPU, exports every symbol the
+headers declare, and its host planner (row a0) equals the oracle planner bit-exactly."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from paper_2402_15627_b200 import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    B.build()
+    from paper_2402_15627_b200 import lamb
+    return lamb
+
+
+def declared_functions():
+    names = []
+    for h in ("lamb.h", "lamb_synth.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names += re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s+(lamb_[a-z_0-9]+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_exports_every_declared_symbol(L):
+    names = declared_functions()
+    assert len(names) >= 20
+    so = ctypes.CDLL(L.LIB_PATH)
+    for n in names:
+        assert hasattr(so, n), n
+    assert set(names) == set(L.exported_symbols())
+
+
+def test_errors_without_gpu_are_reported(L):
+    # argument validation happens before any device call
+    v = L.lamb_group(1e-3, 0.9, 1.5, 1e-6, 0.0, 1, 1)   # beta2 out of range
+    t = (L.lamb_tensor * 1)(L.lamb_tensor(10, 0, 0))
+    cfg = L.lamb_config(1, 0, 0, 1, 0, 0.0, 0)
+    h = ctypes.c_void_p()
+    st = L.lamb_create(t, 1, (L.lamb_group * 1)(v), 1, ctypes.byref(cfg), None, ctypes.byref(h))
+    assert st == L.LAMB_EINVAL and b"beta2" in L.lamb_last_error(None)
+    with pytest.raises(L.LambError):
+        L.host_plan([5, 0], 1, 0)
+    with pytest.raises(L.LambError):
+        L.host_plan([5], 9, 0)
+    with pytest.raises(L.LambError):
+        L.host_plan([5], 2, 2)
+
+
+def compare(L, numels, D, cap):
+    op = oracle.plan(numels, D, cap)
+    for r in range(D):
+        lp = L.host_plan(numels, D, r, cap)
+        assert lp.flat_size == op.flat_size and lp.shard_size == op.shard_size
+        assert lp.tensor_off.tolist() == op.tensor_off
+        assert lp.tensor_bucket.tolist() == op.tensor_bucket
+        assert [tuple(b) for b in lp.buckets.tolist()] == op.buckets
+        assert [tuple(s) for s in lp.segments.tolist()] == op.segments[r]
+        assert lp.straddlers.tolist() == op.straddlers
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_planner_bit_exact_vs_oracle(L, name):
+    wl = W.get(name)
+    numels = [t.numel for t in wl.tensors]
+    Ds = (1, 2, 4, 8) if name != "530b_stress" else (8,)
+    for D in Ds:
+        compare(L, numels, D, wl.cap)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_planner_bit_exact_random(L, seed):
+    rng = np.random.default_rng(1000 + seed)
+    numels = [t.numel for t in W.random_table(rng, int(rng.integers(1, 80)), max_numel=5000,
+                                              p_big=0.1, big=50000)]
+    cap = int(rng.choice([0, 1, 64, 1000, 8192, 30000]))
+    for D in range(1, 9):
+        compare(L, numels, D, cap if cap else 40_000_000)

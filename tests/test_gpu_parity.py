@@ -1,0 +1,195 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded
+inputs.  Needs a B200; run with `pytest -m gpu`."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from gpu_common import compare_state, run_gpu, spec_of
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def lamb():
+    from paper_2402_15627_b200 import build
+    build.build()
+    from paper_2402_15627_b200 import lamb as L
+    return L
+
+
+def test_device_philox_known_answers(lamb):
+    kat = json.load(open(os.path.join(GOLD, "philox_kat.json")))
+    for ctr, key, exp in kat["vectors"]:
+        assert lamb.device_philox([int(x, 16) for x in ctr], [int(x, 16) for x in key]) == \
+            [int(x, 16) for x in exp]
+
+
+def test_generator_matches_oracle_bit_exact(lamb):
+    wl = W.toy()
+    L = run_gpu(wl, steps=0)
+    L.synth_grads(spec_of(wl), wl.seed, 1, 3)
+    g = L.grad_buffer().float().cpu().numpy().astype(np.float64)
+    w = L.get_state(lamb.LAMB_BUF_W).astype(np.float64)
+    for i, ts in enumerate(wl.tensors):
+        o = int(L.plan.tensor_off[i])
+        assert np.array_equal(g[o:o + ts.numel], oracle.gen_grads(wl.seed, 1, i, 3, ts.gexp, ts.numel))
+        assert np.array_equal(w[o:o + ts.numel], oracle.gen_weights(wl.seed, i, ts.init, ts.numel))
+        end = int(L.plan.tensor_off[i + 1]) if i + 1 < len(wl.tensors) else L.plan.flat_size
+        assert not g[o + ts.numel:end].any()          # padding stays zero
+    L.close()
+
+
+@pytest.mark.parametrize("steps", [1, 10])
+def test_toy_parity(lamb, steps):
+    wl = W.toy()
+    L = run_gpu(wl, steps=steps)
+    orc = oracle.OracleRun(wl, world_size=1, mode=oracle.PER_RANK)
+    for t in range(1, steps + 1):
+        orc.step(t)
+    compare_state(L, orc, steps)
+    L.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_ragged_tables(lamb, seed):
+    rng = np.random.default_rng(500 + seed)
+    tensors = W.random_table(rng, 40, max_numel=3000, p_big=0.15, big=60_000)
+    tensors.append(W.TensorSpec("one", 1, W.NO_DECAY, W.INIT_UNIFORM, W.GEXP_VECTOR))
+    wl = W.Workload("rand", 20 + seed, tensors, W.default_groups(lr=2.0 ** -7))
+    cap = int(rng.choice([1, 4096, 20_000]))
+    L = run_gpu(wl, steps=3, cap=cap)
+    orc = oracle.OracleRun(wl, world_size=1)
+    for t in (1, 2, 3):
+        orc.step(t)
+    compare_state(L, orc, 3)
+    L.close()
+
+
+def test_group_variants(lamb):
+    """adapt=0 (AdamW), no bias correction, lr=0, large weight decay."""
+    rng = np.random.default_rng(9)
+    tensors = [W.TensorSpec(f"x{k}", int(rng.integers(1, 9000)), k, W.INIT_UNIFORM, W.GEXP_MATRIX)
+               for k in range(4)]
+    groups = [W.GroupSpec(lr=2.0 ** -7, weight_decay=0.01, adapt=0),
+              W.GroupSpec(lr=2.0 ** -7, weight_decay=0.0, bias_correction=0),
+              W.GroupSpec(lr=0.0, weight_decay=0.01),
+              W.GroupSpec(lr=2.0 ** -8, weight_decay=0.5, beta1=0.8, beta2=0.99, eps=1e-8)]
+    wl = W.Workload("groups", 30, tensors, groups)
+    L = run_gpu(wl, steps=4)
+    orc = oracle.OracleRun(wl, world_size=1)
+    for t in range(1, 5):
+        orc.step(t)
+    compare_state(L, orc, 4)
+    L.close()
+
+
+def test_determinism_bitwise(lamb):
+    """H13: two runs give bitwise-identical w, m, v, params (no float atomics)."""
+    rng = np.random.default_rng(77)
+    wl = W.Workload("det", 40, W.random_table(rng, 30, max_numel=20000), W.default_groups())
+    outs = []
+    for _ in range(2):
+        L = run_gpu(wl, steps=3, cap=50_000)
+        outs.append([L.get_state(k) for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V)]
+                    + [L.param_buffer().view(torch.int16).cpu().numpy()])
+        L.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def test_zero_grad_tensor_and_zero_weights(lamb):
+    """Z9 fallbacks on the GPU: ||w|| = 0 (zero-init biases at step 1) and ||u|| = 0."""
+    tensors = [W.TensorSpec("zb", 100, W.NO_DECAY, W.INIT_ZERO, W.GEXP_VECTOR),
+               W.TensorSpec("m", 4096, W.DECAY, W.INIT_UNIFORM, W.GEXP_MATRIX)]
+    wl = W.Workload("z", 41, tensors, W.default_groups(lr=2.0 ** -7))
+    L = run_gpu(wl, steps=1)
+    _, _, ratio = L.tensor_stats()
+    assert ratio[0] == 1.0
+    orc = oracle.OracleRun(wl)
+    orc.step(1)
+    compare_state(L, orc, 1)
+    # ||u|| = 0: zero grads and zero decay -> unchanged weights, ratio 1
+    L.grad_buffer().zero_()
+    wl2 = W.Workload("z2", 42, [W.TensorSpec("a", 1000, 0, W.INIT_UNIFORM, W.GEXP_VECTOR)],
+                     [W.GroupSpec(weight_decay=0.0)])
+    L2 = run_gpu(wl2, steps=0)
+    w0 = L2.get_state(lamb.LAMB_BUF_W).copy()
+    L2.step(1)
+    torch.cuda.synchronize()
+    assert np.array_equal(L2.get_state(lamb.LAMB_BUF_W), w0)
+    assert L2.tensor_stats()[2][0] == 1.0
+    L.close()
+    L2.close()
+
+
+def test_abi_errors_on_gpu(lamb):
+    wl = W.toy()
+    L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups)
+    with pytest.raises(lamb.LambError) as e:
+        L.step(1)                      # master not set
+    assert e.value.status == lamb.LAMB_ESTATE
+    L.synth_init(spec_of(wl), wl.seed)
+    with pytest.raises(lamb.LambError) as e:
+        L.step(0)
+    assert e.value.status == lamb.LAMB_EINVAL
+    L.close()
+
+
+def test_set_master_and_step_host(lamb):
+    """lamb_set_master from a host array + the host-buffer e2e entry point."""
+    wl = W.toy()
+    L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups)
+    flat = torch.zeros(L.plan.flat_size, dtype=torch.float32)
+    orc = oracle.OracleRun(wl)
+    for i, ts in enumerate(wl.tensors):
+        o = int(L.plan.tensor_off[i])
+        flat[o:o + ts.numel] = torch.from_numpy(orc.w[i]).float()
+    L.set_master(flat)
+    L.synth_grads(spec_of(wl), wl.seed, 1, 1)
+    hg = L.grad_buffer().cpu().pin_memory()
+    hp = torch.empty(L.plan.flat_size, dtype=torch.bfloat16).pin_memory()
+    L.grad_buffer().zero_()
+    L.step_host(hg, hp, 1)
+    torch.cuda.synchronize()
+    orc.step(1)
+    compare_state(L, orc, 1)
+    assert torch.equal(hp.view(torch.int16), L.param_buffer().cpu().view(torch.int16))
+    L.close()
+
+
+def test_gpt13b_layout_1p3b_full_size_sampled(lamb):
+    """BASELINE configs[1] at full size in the bench launch configuration: sampled tensors
+    against the oracle (every tensor's result depends only on its own data), and the
+    step-size invariant ||dw|| = lr ||w|| (H7) on every adapted tensor."""
+    wl = W.gpt_1p3b()
+    from paper_2402_15627_b200 import lamb as Lm
+    L = Lm.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, timing=True)
+    spec = spec_of(wl)
+    L.synth_init(spec, wl.seed)
+    L.synth_grads(spec, wl.seed, 1, 1)
+    w_before = L.state_buffer(Lm.LAMB_BUF_W).clone()
+    L.step(1)
+    torch.cuda.synchronize()
+    w_after = L.state_buffer(Lm.LAMB_BUF_W)
+    ids = [0] + list(range(1, 13)) + [len(wl.tensors) - 2, len(wl.tensors) - 1]
+    orc = oracle.OracleRun(wl, world_size=1, tensor_ids=ids)
+    orc.step(1)
+    compare_state(L, orc, 1, ids=ids)
+    # H7 on every tensor, computed with torch on the device from the library's state
+    lr = float(np.float32(W.LR_BENCH))
+    for (i, soff, toff, ln) in L.plan.segments.tolist():
+        a = w_before[soff:soff + ln].double()
+        b = w_after[soff:soff + ln].double()
+        wn = torch.linalg.vector_norm(a).item()
+        if wn == 0.0:
+            continue
+        dn = torch.linalg.vector_norm(b - a).item()
+        assert abs(dn - lr * wn) <= 2e-5 * lr * wn + 1e-9, (i, dn, lr * wn)
+    L.close()
