@@ -14,23 +14,15 @@
 // All three are HBM/NVLink streaming kernels (~1 flop/B): no tensor cores.  Design for B200:
 // 128-bit coalesced loads with L1::no_allocate, several independent chunks per lane in
 // flight, a persistent grid of (148 x resident CTAs) warps walking the item table.
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
 #include "lamb_kernels.cuh"
 
 namespace lamb {
 
 // ------------------------------------------------------------ memory helpers
-__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
-    float4 r;
-    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-    return r;
-}
-__device__ __forceinline__ float4 ld_ro_f4(const float* p) {
-    float4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-    return r;
-}
 __device__ __forceinline__ uint2 ld_ro_u2(const void* p) {
     uint2 r;
     asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
@@ -53,16 +45,30 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 // ------------------------------------------------------------ the LAMB element math
-// Both passes call exactly these functions with explicit-rounding intrinsics (no FMA
-// contraction, no fast-math), so pass B recomputes the same u bits pass A normed.
+// Both passes call exactly these functions.  Every operation is an explicit-rounding intrinsic
+// or a fixed PTX instruction (no FMA contraction, no fast-math, no data-dependent branches),
+// so pass B recomputes bit-for-bit the u that pass A normed.  sqrt/rcp use the branch-free
+// MUFU approximations (<= 1-2 ulp; the IEEE-rounded sequences carry slow-path branches that
+// made the passes issue-bound, see profiles/r01_notes.md); u stays within ~4 ulp of the
+// correctly rounded fp32 value, far inside the 1e-5 contract.
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ void adam_moments(float g, float& m, float& v, const GroupConst& G) {
     m = __fmaf_rn(G.b1, m, __fmul_rn(G.omb1, g));
     v = __fmaf_rn(G.b2, v, __fmul_rn(G.omb2, __fmul_rn(g, g)));
 }
 __device__ __forceinline__ float lamb_update(float m, float v, float w, const GroupConst& G) {
     const float mh = __fmul_rn(m, G.c1);
-    const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(v, G.c2)), G.eps);
-    return __fmaf_rn(G.wd, w, __fdiv_rn(mh, den));
+    const float den = __fadd_rn(sqrt_approx(__fmul_rn(v, G.c2)), G.eps);
+    return __fmaf_rn(G.wd, w, __fmul_rn(mh, rcp_approx(den)));
 }
 
 __device__ __forceinline__ double warp_sum(double x) {
@@ -71,80 +77,113 @@ __device__ __forceinline__ double warp_sum(double x) {
     return x;
 }
 
+// gradient chunk (4 elements) at flat offset e: fp32 sum over NS bf16 sources in rank order
+template <int NS>
+__device__ __forceinline__ float4 load_grad(const StepParams& P, const Item& I, int64_t e) {
+    if constexpr (NS == 0) {
+        return __ldcs(reinterpret_cast<const float4*>(P.g32 + I.shard_off + e));
+    } else {
+        uint2 raw[NS];
+#pragma unroll
+        for (int j = 0; j < NS; ++j) raw[j] = __ldcs(reinterpret_cast<const uint2*>(P.gsrc[j] + I.flat_off + e));
+        // fp32 accumulation in fixed rank order j = 0..D-1 (reading Z11)
+        float4 s = make_float4(bf_lo(raw[0].x), bf_hi(raw[0].x), bf_lo(raw[0].y), bf_hi(raw[0].y));
+#pragma unroll
+        for (int j = 1; j < NS; ++j) {
+            s.x = __fadd_rn(s.x, bf_lo(raw[j].x));
+            s.y = __fadd_rn(s.y, bf_hi(raw[j].x));
+            s.z = __fadd_rn(s.z, bf_lo(raw[j].y));
+            s.w = __fadd_rn(s.w, bf_hi(raw[j].y));
+        }
+        return s;
+    }
+}
+
+// moments + update + squares of one 4-element chunk (registers in, registers out)
+__device__ __forceinline__ void chunk_a(float4 g, float4& m, float4& v, const float4 w, float gs,
+                                        const GroupConst& G, float& sw, float& su) {
+    float gg[4] = {g.x, g.y, g.z, g.w}, mm[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
+    const float ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        adam_moments(__fmul_rn(gg[q], gs), mm[q], vv[q], G);
+        const float u = lamb_update(mm[q], vv[q], ww[q], G);
+        sw = __fmaf_rn(ww[q], ww[q], sw);
+        su = __fmaf_rn(u, u, su);
+    }
+    m = make_float4(mm[0], mm[1], mm[2], mm[3]);
+    v = make_float4(vv[0], vv[1], vv[2], vv[3]);
+}
+
 // ------------------------------------------------------------ pass A
 // NS > 0: NS bf16 sources (fused reduce-scatter, NS = D); NS == 0: fp32 reduced shard (g32).
-template <int NS, int U>
-__global__ void __launch_bounds__(kThreads) pass_a_kernel(const __grid_constant__ StepParams P) {
+// Lane l of the item's warp handles chunks l, l+32, ...; U chunks per lane are loaded before
+// any is used (U x 56 B in flight per lane).  Norm partials: fp32 over the U x 4 elements of
+// one block, then fp64 (reading Z16).
+template <int NS, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) pass_a_kernel(const __grid_constant__ StepParams P) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
+    const float gs = P.grad_scale;
     for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
         const Item I = P.items[it];
         const GroupConst& G = P.groups[I.group];
-        float* const wp = P.w + I.shard_off;
-        float* const mp = P.m + I.shard_off;
-        float* const vp = P.v + I.shard_off;
-        double sw = 0.0, su = 0.0;
-        for (int c0 = 0; c0 < I.n_chunk; c0 += 32 * U) {
+        float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
+        float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
+        const float4* __restrict__ wp = reinterpret_cast<const float4*>(P.w + I.shard_off);
+        const int n = I.n_chunk;
+        double dw = 0.0, du = 0.0;
+        int c = lane;
+        for (; c + 32 * (U - 1) < n; c += 32 * U) {
             float4 g[U], m[U], v[U], w[U];
 #pragma unroll
             for (int k = 0; k < U; ++k) {
-                const int c = c0 + k * 32 + lane;
-                if (c < I.n_chunk) {
-                    const int64_t e = 4 * (int64_t)c;
-                    m[k] = ld_stream_f4(mp + e);
-                    v[k] = ld_stream_f4(vp + e);
-                    w[k] = ld_ro_f4(wp + e);
-                    if constexpr (NS == 0) {
-                        g[k] = ld_ro_f4(P.g32 + I.shard_off + e);
-                    } else {
-                        uint2 raw[NS];
-#pragma unroll
-                        for (int j = 0; j < NS; ++j) raw[j] = ld_ro_u2(P.gsrc[j] + I.flat_off + e);
-                        // fp32 accumulation in fixed rank order j = 0..D-1 (reading Z11)
-                        float4 s = make_float4(bf_lo(raw[0].x), bf_hi(raw[0].x),
-                                               bf_lo(raw[0].y), bf_hi(raw[0].y));
-#pragma unroll
-                        for (int j = 1; j < NS; ++j) {
-                            s.x = __fadd_rn(s.x, bf_lo(raw[j].x));
-                            s.y = __fadd_rn(s.y, bf_hi(raw[j].x));
-                            s.z = __fadd_rn(s.z, bf_lo(raw[j].y));
-                            s.w = __fadd_rn(s.w, bf_hi(raw[j].y));
-                        }
-                        g[k] = s;
-                    }
-                }
+                const int ck = c + 32 * k;
+                g[k] = load_grad<NS>(P, I, 4 * (int64_t)ck);
+                m[k] = __ldcs(mp + ck);
+                v[k] = __ldcs(vp + ck);
+                w[k] = __ldcs(wp + ck);
             }
+            float sw = 0.f, su = 0.f;
 #pragma unroll
             for (int k = 0; k < U; ++k) {
-                const int c = c0 + k * 32 + lane;
-                if (c < I.n_chunk) {
-                    const int64_t e = 4 * (int64_t)c;
-                    float gs[4] = {g[k].x, g[k].y, g[k].z, g[k].w};
-                    float ms[4] = {m[k].x, m[k].y, m[k].z, m[k].w};
-                    float vs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-                    const float ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        adam_moments(__fmul_rn(gs[q], P.grad_scale), ms[q], vs[q], G);
-                        const float u = lamb_update(ms[q], vs[q], ws[q], G);
-                        sw = fma((double)ws[q], (double)ws[q], sw);
-                        su = fma((double)u, (double)u, su);
-                    }
-                    st_f4(mp + e, make_float4(ms[0], ms[1], ms[2], ms[3]));
-                    st_f4(vp + e, make_float4(vs[0], vs[1], vs[2], vs[3]));
-                }
+                chunk_a(g[k], m[k], v[k], w[k], gs, G, sw, su);
+                __stcs(mp + c + 32 * k, m[k]);
+                __stcs(vp + c + 32 * k, v[k]);
             }
+            dw += (double)sw;
+            du += (double)su;
         }
-        sw = warp_sum(sw);
-        su = warp_sum(su);
-        if (lane == 0) P.partials[it] = make_double2(sw, su);
+        for (; c < n; c += 32) {
+            float4 g = load_grad<NS>(P, I, 4 * (int64_t)c), m = __ldcs(mp + c), v = __ldcs(vp + c);
+            const float4 w = __ldcs(wp + c);
+            float sw = 0.f, su = 0.f;
+            chunk_a(g, m, v, w, gs, G, sw, su);
+            __stcs(mp + c, m);
+            __stcs(vp + c, v);
+            dw += (double)sw;
+            du += (double)su;
+        }
+        dw = warp_sum(dw);
+        du = warp_sum(du);
+        if (lane == 0) P.partials[it] = make_double2(dw, du);
     }
 }
 
 // ------------------------------------------------------------ pass B
-template <int ND, int U>
-__global__ void __launch_bounds__(kThreads) pass_b_kernel(const __grid_constant__ StepParams P) {
+__device__ __forceinline__ uint2 chunk_b(const float4 m, const float4 v, float4& w, float scale,
+                                         const GroupConst& G) {
+    const float mm[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
+    float ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ww[q] = __fmaf_rn(-scale, lamb_update(mm[q], vv[q], ww[q], G), ww[q]);
+    w = make_float4(ww[0], ww[1], ww[2], ww[3]);
+    return make_uint2(pack_bf16x2(ww[0], ww[1]), pack_bf16x2(ww[2], ww[3]));
+}
+
+template <int ND, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) pass_b_kernel(const __grid_constant__ StepParams P) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
@@ -152,38 +191,35 @@ __global__ void __launch_bounds__(kThreads) pass_b_kernel(const __grid_constant_
         const Item I = P.items[it];
         const GroupConst& G = P.groups[I.group];
         const float scale = P.scale[I.tensor];
-        float* const wp = P.w + I.shard_off;
-        const float* const mp = P.m + I.shard_off;
-        const float* const vp = P.v + I.shard_off;
-        for (int c0 = 0; c0 < I.n_chunk; c0 += 32 * U) {
+        float4* __restrict__ wp = reinterpret_cast<float4*>(P.w + I.shard_off);
+        const float4* __restrict__ mp = reinterpret_cast<const float4*>(P.m + I.shard_off);
+        const float4* __restrict__ vp = reinterpret_cast<const float4*>(P.v + I.shard_off);
+        const int n = I.n_chunk;
+        int c = lane;
+        for (; c + 32 * (U - 1) < n; c += 32 * U) {
             float4 m[U], v[U], w[U];
 #pragma unroll
             for (int k = 0; k < U; ++k) {
-                const int c = c0 + k * 32 + lane;
-                if (c < I.n_chunk) {
-                    const int64_t e = 4 * (int64_t)c;
-                    m[k] = ld_ro_f4(mp + e);
-                    v[k] = ld_ro_f4(vp + e);
-                    w[k] = ld_stream_f4(wp + e);
-                }
+                m[k] = __ldcs(mp + c + 32 * k);
+                v[k] = __ldcs(vp + c + 32 * k);
+                w[k] = __ldcs(wp + c + 32 * k);
             }
 #pragma unroll
             for (int k = 0; k < U; ++k) {
-                const int c = c0 + k * 32 + lane;
-                if (c < I.n_chunk) {
-                    const int64_t e = 4 * (int64_t)c;
-                    const float ms[4] = {m[k].x, m[k].y, m[k].z, m[k].w};
-                    const float vs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-                    float ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+                const uint2 pb = chunk_b(m[k], v[k], w[k], scale, G);
+                __stcs(wp + c + 32 * k, w[k]);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        ws[q] = __fmaf_rn(-scale, lamb_update(ms[q], vs[q], ws[q], G), ws[q]);
-                    st_f4(wp + e, make_float4(ws[0], ws[1], ws[2], ws[3]));
-                    const uint2 pb = make_uint2(pack_bf16x2(ws[0], ws[1]), pack_bf16x2(ws[2], ws[3]));
-#pragma unroll
-                    for (int j = 0; j < ND; ++j) st_u2(P.pdst[j] + I.flat_off + e, pb);
-                }
+                for (int j = 0; j < ND; ++j)
+                    __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c + 32 * k, pb);
             }
+        }
+        for (; c < n; c += 32) {
+            const float4 m = __ldcs(mp + c), v = __ldcs(vp + c);
+            float4 w = __ldcs(wp + c);
+            const uint2 pb = chunk_b(m, v, w, scale, G);
+            __stcs(wp + c, w);
+#pragma unroll
+            for (int j = 0; j < ND; ++j) __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c, pb);
         }
     }
     if constexpr (ND > 1) __threadfence_system();   // peer stores visible before the barrier
@@ -200,30 +236,52 @@ __device__ __forceinline__ void trust_ratio(double w2, double u2, const GroupCon
     P.ratio[tensor] = (float)ratio;
 }
 
-// One warp per segment: fixed-order sum of its item partials (lane-strided, then xor tree).
-__global__ void __launch_bounds__(256) finalize_segments_kernel(const __grid_constant__ FinalizeParams P) {
-    const int lane = threadIdx.x & 31;
-    const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (s >= P.n_segs) return;
-    const SegDesc S = P.segs[s];
+// One CTA per segment: thread t sums items t, t+256, ... in order (8 loads in flight), then a
+// fixed shared-memory tree.  Deterministic, no atomics.
+constexpr int kFinThreads = 256;
+__global__ void __launch_bounds__(kFinThreads) finalize_segments_kernel(const __grid_constant__ FinalizeParams P) {
+    __shared__ double2 red[kFinThreads];
+    const int tid = threadIdx.x;
+    const SegDesc S = P.segs[blockIdx.x];
     double w2 = 0.0, u2 = 0.0;
-    for (int64_t i = S.item_begin + lane; i < S.item_end; i += 32) {
+    int64_t i = S.item_begin + tid;
+    for (; i + 7 * kFinThreads < S.item_end; i += 8 * kFinThreads) {
+        double2 q[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q[k] = P.partials[i + k * kFinThreads];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            w2 += q[k].x;
+            u2 += q[k].y;
+        }
+    }
+    for (; i < S.item_end; i += kFinThreads) {
         const double2 q = P.partials[i];
         w2 += q.x;
         u2 += q.y;
     }
-    w2 = warp_sum(w2);
-    u2 = warp_sum(u2);
-    if (lane == 0) {
+    red[tid] = make_double2(w2, u2);
+    __syncthreads();
+#pragma unroll
+    for (int o = kFinThreads / 2; o > 0; o >>= 1) {
+        if (tid < o) {
+            red[tid].x += red[tid + o].x;
+            red[tid].y += red[tid + o].y;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        w2 = red[0].x;
+        u2 = red[0].y;
         if (S.strad_slot < 0) {
             trust_ratio(w2, u2, P.groups[S.group], S.tensor, P);
         } else {
             const double2 val = make_double2(w2, u2);
             for (int j = 0; j < P.world; ++j)
                 P.xrow[j][(int64_t)P.rank * P.n_strad + S.strad_slot] = val;
+            if (P.world > 1) __threadfence_system();
         }
     }
-    if (P.world > 1) __threadfence_system();
 }
 
 // One thread per straddler this rank touches: sum the D rows in rank order.
@@ -302,13 +360,32 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* _
 }
 
 // ------------------------------------------------------------ host launchers
-template <int NS>
-static constexpr int unroll_a() { return NS <= 1 ? 4 : 2; }
+// Variant table: unroll U and min-CTAs-per-SM (register cap) per pass.  Defaults from the
+// r01 sweep (profiles/); LAMB_TUNE="ua=U,ma=M,ub=U,mb=M" overrides for tuning runs.
+struct Tune {
+    int ua = 4, ma = 2, ub = 4, mb = 2;
+};
+static Tune g_tune = [] {
+    Tune t;
+    if (const char* e = getenv("LAMB_TUNE")) {
+        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d", &t.ua, &t.ma, &t.ub, &t.mb);
+    }
+    return t;
+}();
 
+template <int NS, int U, int M>
+static cudaError_t pass_a_v(const StepParams& p, int grid, cudaStream_t s) {
+    pass_a_kernel<NS, U, M><<<grid, kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
 template <int NS>
 static cudaError_t pass_a_ns(const StepParams& p, int grid, cudaStream_t s) {
-    pass_a_kernel<NS, unroll_a<NS>()><<<grid, kThreads, 0, s>>>(p);
-    return cudaGetLastError();
+    const Tune& t = g_tune;
+    if (t.ua == 2 && t.ma == 4) return pass_a_v<NS, 2, 4>(p, grid, s);
+    if (t.ua == 2 && t.ma == 3) return pass_a_v<NS, 2, 3>(p, grid, s);
+    if (t.ua == 4 && t.ma == 3) return pass_a_v<NS, 4, 3>(p, grid, s);
+    if (t.ua == 4 && t.ma == 4) return pass_a_v<NS, 4, 4>(p, grid, s);
+    return pass_a_v<NS, 4, 2>(p, grid, s);
 }
 
 cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int grid, cudaStream_t s) {
@@ -327,10 +404,19 @@ cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int grid, cud
     return cudaErrorInvalidValue;
 }
 
+template <int ND, int U, int M>
+static cudaError_t pass_b_v(const StepParams& p, int grid, cudaStream_t s) {
+    pass_b_kernel<ND, U, M><<<grid, kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
 template <int ND>
 static cudaError_t pass_b_nd(const StepParams& p, int grid, cudaStream_t s) {
-    pass_b_kernel<ND, 4><<<grid, kThreads, 0, s>>>(p);
-    return cudaGetLastError();
+    const Tune& t = g_tune;
+    if (t.ub == 2 && t.mb == 4) return pass_b_v<ND, 2, 4>(p, grid, s);
+    if (t.ub == 2 && t.mb == 3) return pass_b_v<ND, 2, 3>(p, grid, s);
+    if (t.ub == 4 && t.mb == 3) return pass_b_v<ND, 4, 3>(p, grid, s);
+    if (t.ub == 4 && t.mb == 4) return pass_b_v<ND, 4, 4>(p, grid, s);
+    return pass_b_v<ND, 4, 2>(p, grid, s);
 }
 
 cudaError_t launch_pass_b(const StepParams& p, int ndst, int grid, cudaStream_t s) {
@@ -358,19 +444,32 @@ static int occupancy_grid(int device, K kernel) {
 }
 
 int pass_grid(int device, int nsrc, bool g32, bool pass_b, int ndst) {
-    // All variants share the launch shape; size by the heaviest register user of each pass.
-    if (pass_b) return occupancy_grid(device, pass_b_kernel<8, 4>);
-    (void)nsrc;
+    // persistent grid: SMs x resident CTAs of the variant that will run
     (void)g32;
-    (void)ndst;
-    return occupancy_grid(device, pass_a_kernel<8, unroll_a<8>()>);
+    const Tune& t = g_tune;
+    auto pick_a = [&](auto ns) -> int {
+        constexpr int NS = decltype(ns)::value;
+        if (t.ua == 2 && t.ma == 4) return occupancy_grid(device, pass_a_kernel<NS, 2, 4>);
+        if (t.ua == 2 && t.ma == 3) return occupancy_grid(device, pass_a_kernel<NS, 2, 3>);
+        if (t.ua == 4 && t.ma == 3) return occupancy_grid(device, pass_a_kernel<NS, 4, 3>);
+        if (t.ua == 4 && t.ma == 4) return occupancy_grid(device, pass_a_kernel<NS, 4, 4>);
+        return occupancy_grid(device, pass_a_kernel<NS, 4, 2>);
+    };
+    auto pick_b = [&](auto nd) -> int {
+        constexpr int ND = decltype(nd)::value;
+        if (t.ub == 2 && t.mb == 4) return occupancy_grid(device, pass_b_kernel<ND, 2, 4>);
+        if (t.ub == 2 && t.mb == 3) return occupancy_grid(device, pass_b_kernel<ND, 2, 3>);
+        if (t.ub == 4 && t.mb == 3) return occupancy_grid(device, pass_b_kernel<ND, 4, 3>);
+        if (t.ub == 4 && t.mb == 4) return occupancy_grid(device, pass_b_kernel<ND, 4, 4>);
+        return occupancy_grid(device, pass_b_kernel<ND, 4, 2>);
+    };
+    if (pass_b) return ndst <= 1 ? pick_b(std::integral_constant<int, 1>()) : pick_b(std::integral_constant<int, 8>());
+    return nsrc <= 1 ? pick_a(std::integral_constant<int, 1>()) : pick_a(std::integral_constant<int, 8>());
 }
 
 cudaError_t launch_finalize_segments(const FinalizeParams& p, cudaStream_t s) {
     if (p.n_segs <= 0) return cudaSuccess;
-    const int64_t warps_per_block = 8;
-    const int64_t blocks = (p.n_segs + warps_per_block - 1) / warps_per_block;
-    finalize_segments_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
+    finalize_segments_kernel<<<(unsigned)p.n_segs, kFinThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,108 @@
+"""Multi-GPU parity of the sharded LAMB step against the oracle (launched by torchrun; see
+tests/test_gpu_multi.py).  Every rank checks its own shard pieces of w, m, v against the
+oracle's unsharded LAMB on the DP-mean gradient (ZeRO-2 semantics), that its param
+buffer equals bf16_rne(w) of the OWNER rank for every element (all-gather), and that all ranks'
+param buffers are identical.
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
+        tests/dist_gpu_parity.py --mode fused
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle  # noqa: E402
+import workloads as W  # noqa: E402
+from gpu_common import compare_state, spec_of  # noqa: E402
+
+
+def gather_full_w(L, world):
+    """All ranks' fp32 shards -> full flat fp32 (host), via the plan's slices."""
+    w = torch.from_numpy(L.get_state(2)).cuda()
+    allw = [torch.empty_like(w) for _ in range(world)]
+    dist.all_gather(allw, w)
+    allw = [a.cpu().numpy() for a in allw]
+    full = np.zeros(L.plan.flat_size, np.float32)
+    sb = 0
+    for (base, S, _, _) in L.plan.buckets.tolist():
+        sl = S // world
+        for j in range(world):
+            full[base + j * sl: base + (j + 1) * sl] = allw[j][sb: sb + sl]
+        sb += sl
+    return full
+
+
+def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, check_all_params=True):
+    from paper_2402_15627_b200 import lamb
+    L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
+                  device=local, comm_mode=mode, bucket_cap=cap if cap else wl.cap, pg=dist.group.WORLD)
+    spec = spec_of(wl)
+    L.synth_init(spec, wl.seed)
+    for t in range(1, steps + 1):
+        L.synth_grads(spec, wl.seed, rank + 1, t)
+        L.step(t)
+    torch.cuda.synchronize()
+    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK, tensor_ids=ids)
+    for t in range(1, steps + 1):
+        orc.step(t)
+    worst = compare_state(L, orc, steps, ids=ids, check_params=False)
+    # all-gather: every rank's param buffer == bf16_rne(owner's w) everywhere, identical on all ranks
+    p = L.param_buffer().view(torch.int16)
+    if check_all_params:
+        full = gather_full_w(L, world)
+        exp = oracle.bf16_rne_bits(full.astype(np.float64))
+        got = p.cpu().numpy().view(np.uint16)
+        bad = np.nonzero(got != exp)[0]
+        assert bad.size == 0, f"{name}: param mismatch at {bad[:5]} got {got[bad[:5]]} exp {exp[bad[:5]]}"
+    h = torch.tensor([int(p.long().sum().item()), int((p.long() * torch.arange(p.numel(), device=p.device) % 1000003).sum().item())],
+                     device="cuda")
+    hs = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(hs, h)
+    assert all(torch.equal(x, hs[0]) for x in hs), f"{name}: param buffers differ across ranks"
+    n_strad = len(L.plan.straddlers)
+    L.close()
+    if rank == 0:
+        print(f"[ok] {name} D={world} mode={mode} steps={steps} straddlers={n_strad} "
+              f"max rel err w={worst:.2e}", flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", default="fused", choices=["fused", "nccl"])
+    ap.add_argument("--big", action="store_true", help="also run the 1.3B layout (sampled)")
+    a = ap.parse_args()
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2402_15627_b200 import lamb
+    mode = lamb.LAMB_COMM_FUSED if a.mode == "fused" else lamb.LAMB_COMM_NCCL
+
+    run_case("toy", W.toy(), world, rank, local, mode, 1)
+    run_case("toy10", W.toy(), world, rank, local, mode, 10)
+    rng = np.random.default_rng(321)
+    tensors = W.random_table(rng, 60, max_numel=4000, p_big=0.15, big=50_000)
+    run_case("ragged", W.Workload("ragged", 50, tensors, W.default_groups(lr=2.0 ** -7)), world, rank,
+             local, mode, 3, cap=8192)
+    stress = W.stress_tensors(0, 3000)
+    run_case("stress", W.Workload("stress", 51, stress, W.default_groups()), world, rank, local, mode, 2,
+             cap=100_000)
+    if a.big:
+        wl = W.gpt_1p3b()
+        ids = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 289, 290]
+        run_case("gpt1.3b", wl, world, rank, local, mode, 1, ids=ids, check_all_params=False)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

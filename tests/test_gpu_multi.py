@@ -1,0 +1,39 @@
+"""Multi-GPU parity (FUSED peer-memory path and the NCCL baseline), launched with torchrun,
+one process per GPU.  Skips when fewer than 2 GPUs are visible."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu,
+              pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")]
+
+
+def _torchrun(n, *args, timeout=900):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "tests", "dist_gpu_parity.py"),
+           *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    print(r.stdout[-4000:])
+    print(r.stderr[-4000:])
+    assert r.returncode == 0
+
+
+@pytest.mark.parametrize("mode", ["fused", "nccl"])
+def test_parity_2gpu(mode):
+    _torchrun(2, "--mode", mode)
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs >= 4 GPUs")
+@pytest.mark.parametrize("mode", ["fused", "nccl"])
+def test_parity_4gpu(mode):
+    _torchrun(4, "--mode", mode)
+
+
+@pytest.mark.skipif(NGPU < 8, reason="needs 8 GPUs")
+def test_parity_8gpu_fused():
+    _torchrun(8, "--mode", "fused", "--big")
