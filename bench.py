@@ -262,8 +262,8 @@ def main():
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        d = json.load(open(tp)).get(f"{wl.name}/D{D}/{args.comm}/{dom}")
-        traffic = d
+        d = json.load(open(tp)).get(f"{wl.name}/D{D}/{args.comm if D > 1 else 'fused'}/{dom}")
+        traffic = d["bytes"] if d else None
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
             "algorithmic_bytes_per_launch": bytes_dom, "launch_ms": t_dom,

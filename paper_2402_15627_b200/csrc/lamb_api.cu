@@ -196,10 +196,10 @@ static void free_ctx(lamb_ctx* h) {
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     for (int j = 0; j < h->cfg.world_size && j < LAMB_MAX_RANKS; ++j) {
-        if (j == h->cfg.rank) continue;
-        if (h->peer_grad[j]) cudaIpcCloseMemHandle(h->peer_grad[j]);
-        if (h->peer_param[j]) cudaIpcCloseMemHandle(h->peer_param[j]);
-        if (h->peer_sync[j]) cudaIpcCloseMemHandle(h->peer_sync[j]);
+        // only IPC-opened peer mappings (FUSED mode); other entries alias this rank's buffers
+        if (h->peer_grad[j] && h->peer_grad[j] != h->grad) cudaIpcCloseMemHandle(h->peer_grad[j]);
+        if (h->peer_param[j] && h->peer_param[j] != h->param) cudaIpcCloseMemHandle(h->peer_param[j]);
+        if (h->peer_sync[j] && h->peer_sync[j] != h->sync) cudaIpcCloseMemHandle(h->peer_sync[j]);
     }
     void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->partials, h->segs, h->scale,
                     h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
