@@ -132,7 +132,11 @@ lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void* stream);
 /* COLLECTIVE.  End-to-end variant with HOST buffers: copies `host_grads` (flat bf16,
  * flat_size elements, pinned for full speed) into the grad buffer, runs lamb_step, and
  * copies the full updated bf16 param buffer back into `host_params` (flat_size elements).
- * Stream-ordered; the caller synchronises `stream` before reading host_params. */
+ * The upload runs on an internal copy stream that waits only until the previous step has
+ * released the grad buffer (so it overlaps the previous call's download): `host_grads` must
+ * hold the gradients when the call is made and stay unchanged until `stream` completes.
+ * `stream` completes once host_params holds the params; synchronise it before reading.
+ * EINVAL: null buffers, step < 1.  ESTATE: master not set. */
 lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_params,
                            int64_t step, void* stream);
 

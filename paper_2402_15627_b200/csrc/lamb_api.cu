@@ -74,6 +74,10 @@ struct lamb_ctx {
     int64_t max_bucket = 0;
     std::vector<cudaEvent_t> ev_rs, ev_a, ev_b, ev_up;
     cudaEvent_t ev_start = nullptr, ev_x = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_grad_free = nullptr;                  // grad buffer may be overwritten
+    // lamb_step_host: copy streams and events (created on first use)
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    cudaEvent_t ev_h2d = nullptr, ev_params = nullptr, ev_d2h = nullptr;
     int grid_a = 0, grid_b = 0;
     // synth tables (device)
     int64_t *d_tensor_off = nullptr, *d_numel = nullptr, *d_shard_base = nullptr,
@@ -210,9 +214,10 @@ static void free_ctx(lamb_ctx* h) {
     if (h->err_flag_host) cudaFreeHost(h->err_flag_host);
     for (auto* vec : {&h->ev_rs, &h->ev_a, &h->ev_b, &h->ev_up, &h->tev})
         for (cudaEvent_t e : *vec) cudaEventDestroy(e);
-    for (cudaEvent_t e : {h->ev_start, h->ev_x, h->ev_done})
+    for (cudaEvent_t e : {h->ev_start, h->ev_x, h->ev_done, h->ev_grad_free, h->ev_h2d, h->ev_params, h->ev_d2h})
         if (e) cudaEventDestroy(e);
-    if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    for (cudaStream_t st : {h->comm_stream, h->h2d_stream, h->d2h_stream})
+        if (st) cudaStreamDestroy(st);
     if (h->comm) ncclCommDestroy(h->comm);
     delete h;
 }
@@ -430,6 +435,7 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
     CUDA_STEP(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
     CUDA_STEP(cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming));
     CUDA_STEP(cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming));
+    CUDA_STEP(cudaEventCreateWithFlags(&h->ev_grad_free, cudaEventDisableTiming));
     for (int j = 0; j < LAMB_MAX_RANKS; ++j) {
         h->peer_grad[j] = h->grad;
         h->peer_param[j] = h->param;
@@ -536,6 +542,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         for (int j = 0; j < D; ++j)
             sp.gsrc[j] = fused ? h->peer_grad[j] : (grads ? (const __nv_bfloat16*)grads : h->grad);
         LAUNCH(h, launch_pass_a(sp, D, false, h->grid_a, s));
+        if (!fused) CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));   // D = 1: grads consumed
         mark(h, 2, s);
         for (int j = 0; j < D; ++j) fp.xrow[j] = h->xbuf(fused ? j : -1);
         LAUNCH(h, launch_finalize_segments(fp, s));
@@ -548,7 +555,11 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         for (int j = 0; j < D; ++j) sp.pdst[j] = fused ? h->peer_param[j] : h->param;
         LAUNCH(h, launch_pass_b(sp, fused ? D : 1, h->grid_b, s));
         mark(h, 5, s);
-        if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+        if (fused) {
+            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+            // every rank finished pass A (peer reads of this rank's grads) before this barrier
+            CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));
+        }
         mark(h, 6, s);
         return LAMB_OK;
     }
@@ -600,6 +611,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     }
     CUDA_TRY(h, cudaEventRecord(h->ev_done, h->comm_stream));
     CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_done, 0));
+    CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));
     mark(h, 5, s);
     mark(h, 6, s);
     return LAMB_OK;
@@ -634,14 +646,35 @@ extern "C" lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void
 
 extern "C" lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_params,
                                       int64_t step, void* stream) {
+    // Pipeline across consecutive calls: the H2D of this step's grads runs on its own copy
+    // stream as soon as the previous step released the grad buffer (ev_grad_free), i.e.
+    // concurrently with the previous step's D2H of params on the other copy engine.  The
+    // step itself is ordered on `stream` after the upload; `stream` completes once the
+    // params are in host_params.
     if (!h || !host_grads || !host_params) return fail(h, LAMB_EINVAL, "null argument");
+    if (step < 1) return fail(h, LAMB_EINVAL, "step must be >= 1");
+    if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step_host before lamb_set_master / lamb_synth_init");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaSetDevice(h->device);
+    if (!h->h2d_stream) {
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_h2d, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_params, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_d2h, cudaEventDisableTiming));
+    }
     const size_t bytes = (size_t)h->plan.flat_size * 2;
-    CUDA_TRY(h, cudaMemcpyAsync(h->grad, host_grads, bytes, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_grad_free, 0));
+    CUDA_TRY(h, cudaMemcpyAsync(h->grad, host_grads, bytes, cudaMemcpyHostToDevice, h->h2d_stream));
+    CUDA_TRY(h, cudaEventRecord(h->ev_h2d, h->h2d_stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_h2d, 0));
     lamb_status st = lamb_step(h, nullptr, step, stream);
     if (st != LAMB_OK) return st;
-    CUDA_TRY(h, cudaMemcpyAsync(host_params, h->param, bytes, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaEventRecord(h->ev_params, s));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->d2h_stream, h->ev_params, 0));
+    CUDA_TRY(h, cudaMemcpyAsync(host_params, h->param, bytes, cudaMemcpyDeviceToHost, h->d2h_stream));
+    CUDA_TRY(h, cudaEventRecord(h->ev_d2h, h->d2h_stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_d2h, 0));
     return LAMB_OK;
 }
 
