@@ -193,3 +193,33 @@ def test_gpt13b_layout_1p3b_full_size_sampled(lamb):
         dn = torch.linalg.vector_norm(b - a).item()
         assert abs(dn - lr * wn) <= 2e-5 * lr * wn + 1e-9, (i, dn, lr * wn)
     L.close()
+
+
+def test_step_host_pipeline_matches_device_steps(lamb):
+    """lamb_step_host over several consecutive steps (upload of step t+1 overlapping the
+    download of step t) is bit-identical to lamb_step on device-resident grads."""
+    wl = W.toy()
+    spec = spec_of(wl)
+    A = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups)
+    B = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups)
+    A.synth_init(spec, wl.seed)
+    B.synth_init(spec, wl.seed)
+    hg = [torch.empty(A.plan.flat_size, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+    hp = [torch.empty(A.plan.flat_size, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+    for t in range(1, 5):
+        A.synth_grads(spec, wl.seed, 1, t)
+        hg[t - 1].copy_(A.grad_buffer())
+    torch.cuda.synchronize()
+    A.grad_buffer().zero_()
+    for t in range(1, 5):
+        A.step_host(hg[t - 1], hp[t - 1], t)        # no sync between calls
+    torch.cuda.synchronize()
+    for t in range(1, 5):
+        B.synth_grads(spec, wl.seed, 1, t)
+        B.step(t)
+        torch.cuda.synchronize()
+        assert torch.equal(hp[t - 1].view(torch.int16), B.param_buffer().cpu().view(torch.int16)), t
+    for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V):
+        assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32))
+    A.close()
+    B.close()
