@@ -172,6 +172,27 @@ lamb_status lamb_get_tensor_stats(lamb_t h, double* w_sq, double* u_sq, float* r
 /* Changes a group's learning rate for subsequent steps (schedules live outside, Z13). */
 lamb_status lamb_set_lr(lamb_t h, int32_t group, float lr);
 
+/* ---------------- checkpoint / resume with reshard (§4.4) ----------------
+ * File format (little endian; one file per checkpoint, written by all ranks at disjoint
+ * offsets): header {char magic[8] = "LAMBCKPT"; u32 version = 1; u32 world size that saved;
+ * i64 n_tensors, step, n_params, data_off} + i64 numel[n_tensors], zero-padded to data_off
+ * (multiple of 4096); then fp32 arrays W, M, V of n_params elements each in table order,
+ * no padding.  Independent of D, bucket cap and alignment: load at any world size. */
+/* COLLECTIVE.  Stage 1 (blocking): copies this rank's w/m/v shard into pinned host staging
+ * (allocated on first use: 12 * shard_size bytes) after the work already on `stream`.
+ * Stage 2 (background host thread): writes this rank's segments into `path` (created if
+ * missing; rank 0 writes the header and sizes the file).  Returns after stage 1; training
+ * may continue.  A second save first waits for the previous one.
+ * EINVAL: null path.  ESTATE: master not set.  ENOMEM: staging allocation. */
+lamb_status lamb_checkpoint_save(lamb_t h, const char* path, int64_t step, void* stream);
+/* Waits for the background write of the last save; EINVAL with the I/O error if it failed. */
+lamb_status lamb_checkpoint_wait(lamb_t h);
+/* COLLECTIVE.  Reads only this rank's segments of W, M, V from `path` (saved at any world
+ * size), uploads them, rebuilds the bf16 param buffer (own slices cast, then all-gathered),
+ * marks the master set and returns the saved step in *step (may be NULL).  Synchronous.
+ * EINVAL: unreadable file, wrong magic/version, or a different parameter table. */
+lamb_status lamb_checkpoint_load(lamb_t h, const char* path, int64_t* step, void* stream);
+
 /* ---------------- measurement (CUDA events, §5.1 P:21-35 style) ---------------- */
 #define LAMB_PH_BARRIER_IN 0   /* cross-GPU "grads ready" barrier (FUSED, D > 1) */
 #define LAMB_PH_PASS_A 1       /* a1+a2: (fused RS) + moments + update + partial norms */

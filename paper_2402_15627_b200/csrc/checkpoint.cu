@@ -1,0 +1,213 @@
+// checkpoint.cu — sharded LAMB state checkpoint / resume with reshard.
+//
+// PAPER.md §4.4: two-stage checkpointing — stage 1, every GPU worker copies its
+// on-chip state into pinned host memory (blocking, "several seconds" thanks to PCIe);
+// stage 2, a background process writes host memory to storage while training continues.
+// Recovery: workers that share a state partition should not all read it; here no
+// rank ever reads more than its own ZeRO-2 partition, and the replicated bf16 params are
+// rebuilt by an all-gather instead of being read D times.
+//
+// File format (little endian, one file per checkpoint, written by all ranks at disjoint
+// offsets): header {magic "LAMBCKPT", u32 version = 1, u32 world size that saved,
+// i64 n_tensors, i64 step, i64 n_params, i64 data_off} + i64 numel[n_tensors], zero-padded to
+// data_off (multiple of 4096); then three fp32 arrays W, M, V of n_params elements each, in
+// table order without padding (tensor i occupies [cum_i, cum_i + numel_i)).  The layout does
+// not depend on D, the bucket cap or alignment, so a checkpoint saved at any world size loads
+// at any other (reshard).
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cstring>
+
+#include "ctx.hpp"
+
+namespace {
+
+constexpr char kMagic[8] = {'L', 'A', 'M', 'B', 'C', 'K', 'P', 'T'};
+constexpr uint32_t kVersion = 1;
+
+struct Header {
+    char magic[8];
+    uint32_t version;
+    uint32_t world_saved;
+    int64_t n_tensors, step, n_params, data_off;
+};
+
+int64_t data_offset(int64_t T) { return (int64_t)((sizeof(Header) + 8 * T + 4095) / 4096 * 4096); }
+
+bool pwrite_all(int fd, const void* buf, size_t n, off_t off) {
+    const char* p = static_cast<const char*>(buf);
+    while (n > 0) {
+        ssize_t k = pwrite(fd, p, n, off);
+        if (k <= 0) return false;
+        p += k;
+        n -= (size_t)k;
+        off += k;
+    }
+    return true;
+}
+
+bool pread_all(int fd, void* buf, size_t n, off_t off) {
+    char* p = static_cast<char*>(buf);
+    while (n > 0) {
+        ssize_t k = pread(fd, p, n, off);
+        if (k <= 0) return false;
+        p += k;
+        n -= (size_t)k;
+        off += k;
+    }
+    return true;
+}
+
+std::vector<int64_t> prefix(const Plan& p) {
+    std::vector<int64_t> cum(p.n_tensors() + 1, 0);
+    for (int64_t i = 0; i < p.n_tensors(); ++i) cum[i + 1] = cum[i] + p.numel[i];
+    return cum;
+}
+
+lamb_status ensure_stage(lamb_ctx* h) {
+    if (!h->ck_stage) {
+        CUDA_TRY(h, cudaHostAlloc(reinterpret_cast<void**>(&h->ck_stage),
+                                  3 * (size_t)h->plan.shard_size * sizeof(float), cudaHostAllocDefault));
+    }
+    return LAMB_OK;
+}
+
+}  // namespace
+
+extern "C" lamb_status lamb_checkpoint_wait(lamb_t h) {
+    if (!h) return lamb_fail(nullptr, LAMB_EINVAL, "null handle");
+    if (h->ck_thread.joinable()) h->ck_thread.join();
+    if (h->ck_status != LAMB_OK) return lamb_fail(h, h->ck_status, h->ck_error);
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_checkpoint_save(lamb_t h, const char* path, int64_t step, void* stream) {
+    if (!h || !path) return lamb_fail(h, LAMB_EINVAL, "null argument");
+    if (!h->master_set) return lamb_fail(h, LAMB_ESTATE, "nothing to save: master not set");
+    lamb_status st = lamb_checkpoint_wait(h);   // one save in flight at a time
+    if (st != LAMB_OK) return st;
+    st = ensure_stage(h);
+    if (st != LAMB_OK) return st;
+    cudaSetDevice(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t n = (size_t)h->plan.shard_size;
+    // stage 1 (blocking): device shards -> pinned host
+    CUDA_TRY(h, cudaMemcpyAsync(h->ck_stage, h->w, n * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaMemcpyAsync(h->ck_stage + n, h->m, n * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaMemcpyAsync(h->ck_stage + 2 * n, h->v, n * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    // stage 2 (background): this rank's segments -> file
+    h->ck_status = LAMB_OK;
+    h->ck_error.clear();
+    std::string file(path);
+    h->ck_thread = std::thread([h, file, step]() {
+        const Plan& p = h->plan;
+        const std::vector<int64_t> cum = prefix(p);
+        const int64_t T = p.n_tensors(), N = cum[T], doff = data_offset(T);
+        auto fail_io = [&](const char* what) {
+            h->ck_status = LAMB_EINVAL;
+            h->ck_error = std::string("checkpoint save: ") + what + " " + file + ": " + strerror(errno);
+        };
+        int fd = open(file.c_str(), O_WRONLY | O_CREAT, 0644);
+        if (fd < 0) return fail_io("open");
+        if (p.rank == 0) {
+            std::vector<char> hdr((size_t)doff, 0);
+            Header H;
+            memcpy(H.magic, kMagic, 8);
+            H.version = kVersion;
+            H.world_saved = (uint32_t)p.world;
+            H.n_tensors = T;
+            H.step = step;
+            H.n_params = N;
+            H.data_off = doff;
+            memcpy(hdr.data(), &H, sizeof(H));
+            memcpy(hdr.data() + sizeof(H), p.numel.data(), 8 * (size_t)T);
+            // never truncate below data written by other ranks: size the file exactly
+            if (ftruncate(fd, doff + 3 * N * 4) != 0 || !pwrite_all(fd, hdr.data(), hdr.size(), 0)) {
+                close(fd);
+                return fail_io("header");
+            }
+        }
+        const size_t sh = (size_t)p.shard_size;
+        for (int64_t k = 0; k < p.n_segments(); ++k) {
+            const int64_t t = p.segments[4 * k], soff = p.segments[4 * k + 1];
+            const int64_t toff = p.segments[4 * k + 2], len = p.segments[4 * k + 3];
+            for (int x = 0; x < 3; ++x) {
+                const off_t off = doff + ((int64_t)x * N + cum[t] + toff) * 4;
+                if (!pwrite_all(fd, h->ck_stage + x * sh + soff, (size_t)len * 4, off)) {
+                    close(fd);
+                    return fail_io("write");
+                }
+            }
+        }
+        if (fdatasync(fd) != 0) {
+            close(fd);
+            return fail_io("fdatasync");
+        }
+        close(fd);
+    });
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_checkpoint_load(lamb_t h, const char* path, int64_t* step, void* stream) {
+    if (!h || !path) return lamb_fail(h, LAMB_EINVAL, "null argument");
+    lamb_status st = lamb_checkpoint_wait(h);
+    if (st != LAMB_OK) return st;
+    const Plan& p = h->plan;
+    const std::vector<int64_t> cum = prefix(p);
+    const int64_t T = p.n_tensors(), N = cum[T];
+    int fd = open(path, O_RDONLY);
+    if (fd < 0) return lamb_fail(h, LAMB_EINVAL, std::string("checkpoint load: open ") + path + ": " + strerror(errno));
+    Header H;
+    std::vector<int64_t> numel(T);
+    bool ok = pread_all(fd, &H, sizeof(H), 0) && memcmp(H.magic, kMagic, 8) == 0 && H.version == kVersion &&
+              H.n_tensors == T && H.n_params == N && H.data_off == data_offset(T) &&
+              pread_all(fd, numel.data(), 8 * (size_t)T, sizeof(H)) && numel == p.numel;
+    if (!ok) {
+        close(fd);
+        return lamb_fail(h, LAMB_EINVAL, std::string("checkpoint load: ") + path +
+                                             " is not a checkpoint of this parameter table");
+    }
+    st = ensure_stage(h);
+    if (st != LAMB_OK) {
+        close(fd);
+        return st;
+    }
+    const size_t sh = (size_t)p.shard_size;
+    memset(h->ck_stage, 0, 3 * sh * sizeof(float));   // padding stays exactly zero
+    for (int64_t k = 0; k < p.n_segments() && ok; ++k) {
+        const int64_t t = p.segments[4 * k], soff = p.segments[4 * k + 1];
+        const int64_t toff = p.segments[4 * k + 2], len = p.segments[4 * k + 3];
+        for (int x = 0; x < 3 && ok; ++x)
+            ok = pread_all(fd, h->ck_stage + x * sh + soff, (size_t)len * 4,
+                           H.data_off + ((int64_t)x * N + cum[t] + toff) * 4);
+    }
+    close(fd);
+    if (!ok) return lamb_fail(h, LAMB_EINVAL, std::string("checkpoint load: short read of ") + path);
+    cudaSetDevice(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(h, cudaMemcpyAsync(h->w, h->ck_stage, sh * 4, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(h, cudaMemcpyAsync(h->m, h->ck_stage + sh, sh * 4, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(h, cudaMemcpyAsync(h->v, h->ck_stage + 2 * sh, sh * 4, cudaMemcpyHostToDevice, s));
+    // params: cast own slices, then all-gather them (ranks never read other partitions)
+    for (int64_t b = 0; b < p.n_buckets(); ++b) {
+        const int64_t base = p.buckets[4 * b], sl = p.buckets[4 * b + 1] / p.world;
+        CUDA_TRY(h, lamb::launch_cast_to_bf16(h->w + p.shard_base[b], h->param + base + (int64_t)p.rank * sl, sl, s));
+        ++h->launches;
+    }
+    if (p.world > 1) {
+        NCCL_TRY(h, ncclGroupStart());
+        for (int64_t b = 0; b < p.n_buckets(); ++b) {
+            const int64_t base = p.buckets[4 * b], sl = p.buckets[4 * b + 1] / p.world;
+            NCCL_TRY(h, ncclAllGather(h->param + base + (int64_t)p.rank * sl, h->param + base, (size_t)sl,
+                                      ncclBfloat16, h->comm, s));
+        }
+        NCCL_TRY(h, ncclGroupEnd());
+    }
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    h->master_set = true;
+    if (step) *step = H.step;
+    return LAMB_OK;
+}

@@ -26,92 +26,21 @@
 #include "lamb_kernels.cuh"
 #include "planner.hpp"
 #include "synth.cuh"
+#include "ctx.hpp"
 
 using namespace lamb;
 
-static thread_local std::string g_last_error;
-
-struct lamb_plan_ctx {
-    Plan plan;
-};
-
-struct lamb_ctx {
-    Plan plan;
-    lamb_config cfg{};
-    std::vector<lamb_group> groups;
-    std::string err;
-    int device = 0;
-    bool master_set = false;
-    int64_t launches = 0;
-    // device buffers (own)
-    __nv_bfloat16* grad = nullptr;     // flat
-    __nv_bfloat16* param = nullptr;    // flat
-    float *w = nullptr, *m = nullptr, *v = nullptr;   // shard
-    Item* items = nullptr;
-    int64_t n_items = 0;
-    std::vector<int64_t> bucket_item_begin;   // [B+1] items of bucket b: [b], [b+1)
-    double2* partials = nullptr;
-    SegDesc* segs = nullptr;
-    float* scale = nullptr;
-    double *w_sq = nullptr, *u_sq = nullptr;
-    float* ratio = nullptr;
-    int32_t *strad_slots = nullptr, *strad_tensor = nullptr, *strad_group = nullptr;
-    int32_t n_local_strad = 0;
-    // sync buffer: [flags uint64 x 8][epoch uint64][pad][xbuf double2 x D x n_strad]
-    char* sync = nullptr;
-    size_t sync_bytes = 0;
-    int* err_flag_host = nullptr;   // host-mapped
-    int* err_flag_dev = nullptr;
-    // peers (FUSED): index j = rank j (own entry = own pointer)
-    __nv_bfloat16* peer_grad[LAMB_MAX_RANKS] = {};
-    __nv_bfloat16* peer_param[LAMB_MAX_RANKS] = {};
-    char* peer_sync[LAMB_MAX_RANKS] = {};
-    // NCCL
-    ncclComm_t comm = nullptr;
-    cudaStream_t comm_stream = nullptr;
-    float* g32 = nullptr;          // NCCL mode: reduced fp32 grad shard
-    float* up32[2] = {nullptr, nullptr};   // NCCL mode: upcast staging, 2 buckets
-    int64_t max_bucket = 0;
-    std::vector<cudaEvent_t> ev_rs, ev_a, ev_b, ev_up;
-    cudaEvent_t ev_start = nullptr, ev_x = nullptr, ev_done = nullptr;
-    cudaEvent_t ev_grad_free = nullptr;                  // grad buffer may be overwritten
-    // lamb_step_host: copy streams and events (created on first use)
-    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-    cudaEvent_t ev_h2d = nullptr, ev_params = nullptr, ev_d2h = nullptr;
-    int grid_a = 0, grid_b = 0;
-    // synth tables (device)
-    int64_t *d_tensor_off = nullptr, *d_numel = nullptr, *d_shard_base = nullptr,
-            *d_bucket_base = nullptr, *d_bucket_slice = nullptr;
-    // timing
-    std::vector<cudaEvent_t> tev;   // [max_steps][LAMB_N_PHASES + 1]
-    int32_t t_max = 0, t_n = 0;
-
-    uint64_t* flags(int j) const { return reinterpret_cast<uint64_t*>(peer_sync[j]); }
-    uint64_t* epoch() const { return reinterpret_cast<uint64_t*>(sync + 8 * LAMB_MAX_RANKS); }
-    double2* xbuf(int j) const {
-        return reinterpret_cast<double2*>((j < 0 ? sync : peer_sync[j]) + 128);
-    }
-};
 
 // ------------------------------------------------------------------ error plumbing
-static lamb_status fail(lamb_ctx* h, lamb_status st, const std::string& msg) {
-    g_last_error = msg;
+static thread_local std::string g_last_error_storage;
+
+lamb_status lamb_fail(lamb_ctx* h, lamb_status st, const std::string& msg) {
+    g_last_error_storage = msg;
     if (h) h->err = msg;
     return st;
 }
-#define CUDA_TRY(h, call)                                                                     \
-    do {                                                                                      \
-        cudaError_t e_ = (call);                                                              \
-        if (e_ != cudaSuccess)                                                                \
-            return fail(h, e_ == cudaErrorMemoryAllocation ? LAMB_ENOMEM : LAMB_ECUDA,        \
-                        std::string(#call) + ": " + cudaGetErrorString(e_));                  \
-    } while (0)
-#define NCCL_TRY(h, call)                                                                     \
-    do {                                                                                      \
-        ncclResult_t r_ = (call);                                                             \
-        if (r_ != ncclSuccess)                                                                \
-            return fail(h, LAMB_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));   \
-    } while (0)
+static inline lamb_status fail(lamb_ctx* h, lamb_status st, const std::string& msg) { return lamb_fail(h, st, msg); }
+#define g_last_error g_last_error_storage
 
 template <typename T>
 static cudaError_t dalloc(T** p, size_t n) {
@@ -197,7 +126,9 @@ static std::string check_group(const lamb_group& g) {
 
 static void free_ctx(lamb_ctx* h) {
     if (!h) return;
+    if (h->ck_thread.joinable()) h->ck_thread.join();
     cudaSetDevice(h->device);
+    if (h->ck_stage) cudaFreeHost(h->ck_stage);
     cudaDeviceSynchronize();
     for (int j = 0; j < h->cfg.world_size && j < LAMB_MAX_RANKS; ++j) {
         // only IPC-opened peer mappings (FUSED mode); other entries alias this rank's buffers

@@ -87,6 +87,9 @@ _SIGS = {
     "lamb_get_state": (_st, [_vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp]),
     "lamb_get_tensor_stats": (_st, [_vp, _vp, _vp, _vp]),
     "lamb_set_lr": (_st, [_vp, ctypes.c_int32, ctypes.c_float]),
+    "lamb_checkpoint_save": (_st, [_vp, ctypes.c_char_p, ctypes.c_int64, _vp]),
+    "lamb_checkpoint_wait": (_st, [_vp]),
+    "lamb_checkpoint_load": (_st, [_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), _vp]),
     "lamb_timing_begin": (_st, [_vp, ctypes.c_int32]),
     "lamb_timing_read": (_st, [_vp, _vp, ctypes.POINTER(ctypes.c_int32)]),
     "lamb_launch_count": (ctypes.c_int64, [_vp]),
@@ -280,6 +283,18 @@ class Lamb:
 
     def set_lr(self, group: int, lr: float) -> None:
         check(lamb_set_lr(self.h, group, lr), self.h)
+
+    # -- checkpoint / resume (two-stage save, reshard on load)
+    def checkpoint_save(self, path: str, step: int, stream=None) -> None:
+        check(lamb_checkpoint_save(self.h, path.encode(), int(step), self._stream(stream)), self.h)
+
+    def checkpoint_wait(self) -> None:
+        check(lamb_checkpoint_wait(self.h), self.h)
+
+    def checkpoint_load(self, path: str, stream=None) -> int:
+        st = ctypes.c_int64()
+        check(lamb_checkpoint_load(self.h, path.encode(), ctypes.byref(st), self._stream(stream)), self.h)
+        return st.value
 
     def timing_begin(self, max_steps: int) -> None:
         check(lamb_timing_begin(self.h, max_steps), self.h)

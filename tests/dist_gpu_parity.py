@@ -74,6 +74,52 @@ def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, chec
               f"max rel err w={worst:.2e}", flush=True)
 
 
+def ckpt_case(world, rank, local, mode):
+    """Checkpoint saved by D ranks; reloaded (a) by D ranks with another bucket cap and
+    (b) by rank 0 alone at D = 1 (reshard); both continue and must match the oracle."""
+    from paper_2402_15627_b200 import lamb
+    rng = np.random.default_rng(88)
+    tensors = W.random_table(rng, 30, max_numel=5000, p_big=0.2, big=30_000)
+    wl = W.Workload("ckd", 71, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    path = f"/tmp/lamb_ckpt_D{world}_{mode}.bin"
+    mk = lambda D, r, cap, pg: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=D,
+                                         rank=r, device=local, comm_mode=mode, bucket_cap=cap, pg=pg)
+    A = mk(world, rank, 8192, dist.group.WORLD)
+    A.synth_init(spec, wl.seed)
+    for t in (1, 2):
+        A.synth_grads(spec, wl.seed, rank + 1, t)
+        A.step(t)
+    A.checkpoint_save(path, 2)
+    A.checkpoint_wait()
+    A.close()
+    dist.barrier()
+    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+    for t in (1, 2, 3):
+        orc.step(t)
+    B = mk(world, rank, 5000, dist.group.WORLD)
+    assert B.checkpoint_load(path) == 2
+    B.synth_grads(spec, wl.seed, rank + 1, 3)
+    B.step(3)
+    torch.cuda.synchronize()
+    compare_state(B, orc, 3, check_params=False)
+    B.close()
+    dist.barrier()
+    if rank == 0:
+        # D = 1 resume of the D-rank checkpoint: the restored state (step 2) must equal the
+        # oracle's (continuing would need the D-rank mean gradient, which one rank's
+        # generator stream cannot reproduce)
+        C = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=0)
+        assert C.checkpoint_load(path) == 2
+        orc2 = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+        for t in (1, 2):
+            orc2.step(t)
+        compare_state(C, orc2, 2)
+        C.close()
+        print(f"[ok] checkpoint D={world} -> D={world} (new cap) -> D=1 reshard", flush=True)
+    dist.barrier()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mode", default="fused", choices=["fused", "nccl"])
@@ -96,6 +142,7 @@ def main():
     stress = W.stress_tensors(0, 3000)
     run_case("stress", W.Workload("stress", 51, stress, W.default_groups()), world, rank, local, mode, 2,
              cap=100_000)
+    ckpt_case(world, rank, local, mode)
     if a.big:
         wl = W.gpt_1p3b()
         ids = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 289, 290]

@@ -223,3 +223,53 @@ def test_step_host_pipeline_matches_device_steps(lamb):
         assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32))
     A.close()
     B.close()
+
+
+def test_checkpoint_resume_and_reshard(lamb, tmp_path):
+    """NEXT #4: two-stage save at step 3; resume in the same layout is bit-identical to an
+    uninterrupted run; resume into a different bucket layout (reshard) matches the oracle;
+    the file holds the oracle's state (independent numpy reader)."""
+    from ckpt_reader import read_checkpoint
+    rng = np.random.default_rng(17)
+    tensors = W.random_table(rng, 25, max_numel=6000, p_big=0.2, big=40_000)
+    wl = W.Workload("ck", 70, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    path = str(tmp_path / "lamb.ckpt")
+    A = run_gpu(wl, steps=3, cap=10_000)
+    A.checkpoint_save(path, 3)
+    for t in (4, 5):                      # training continues while stage 2 writes
+        A.synth_grads(spec, wl.seed, 1, t)
+        A.step(t)
+    A.checkpoint_wait()
+    torch.cuda.synchronize()
+    orc = oracle.OracleRun(wl)
+    for t in (1, 2, 3):
+        orc.step(t)
+    ck = read_checkpoint(path)
+    assert ck["step"] == 3 and list(ck["numel"]) == [t.numel for t in tensors]
+    for i in range(len(tensors)):
+        for name, ref in (("w", orc.w[i]), ("m", orc.m[i]), ("v", orc.v[i])):
+            x = ck[name][i].astype(np.float64)
+            atol = 1e-6 if name == "w" else 1e-6 * np.max(np.abs(ref))
+            assert np.all(np.abs(x - ref) <= atol + 1e-4 * np.abs(ref)), (i, name)
+    for cap in (10_000, 3_000):           # same layout, then a different one
+        B = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=cap)
+        assert B.checkpoint_load(path) == 3
+        for t in (4, 5):
+            B.synth_grads(spec, wl.seed, 1, t)
+            B.step(t)
+        torch.cuda.synchronize()
+        if cap == 10_000:
+            for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V):
+                assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32))
+            assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
+        else:
+            orc2 = oracle.OracleRun(wl)
+            for t in range(1, 6):
+                orc2.step(t)
+            compare_state(B, orc2, 5)
+        B.close()
+    with pytest.raises(lamb.LambError):   # a different parameter table is refused
+        C = lamb.Lamb([(10, 0)], wl.groups)
+        C.checkpoint_load(path)
+    A.close()

@@ -1,0 +1,20 @@
+"""Print a compact table from bench JSON lines (interleaved with {"run"/"tune": ...} markers)."""
+import json
+import sys
+
+for path in sys.argv[1:]:
+    for line in open(path):
+        try:
+            d = json.loads(line)
+        except Exception:
+            continue
+        if "run" in d or "tune" in d:
+            print(d.get("run") or d.get("tune"))
+            continue
+        if "roofline" not in d:
+            print("  ", line[:200])
+            continue
+        r, p = d["roofline"], d["phases_ms"]
+        print("  ms %.3f  %.1f Gp/s  A %.3f ms %.0f GB/s  B %.3f ms %.0f GB/s  nvl-frac %s" % (
+            d["ms_per_step"], d["value"] / 1e9, p["pass_a"], r["pass_a"]["GBps"], p["pass_b"],
+            r["pass_b"]["GBps"], r.get("nvlink", {}).get("frac_step")))
