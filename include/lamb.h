@@ -172,6 +172,28 @@ lamb_status lamb_get_tensor_stats(lamb_t h, double* w_sq, double* u_sq, float* r
 /* Changes a group's learning rate for subsequent steps (schedules live outside, Z13). */
 lamb_status lamb_set_lr(lamb_t h, int32_t group, float lr);
 
+/* ---------------- pre-step: clipping, loss scale, non-finite skip ----
+ * Enabled while max_grad_norm > 0 or inv_loss_scale != 1.  Each step then computes the GLOBAL
+ * norm gn = ||grad_scale * inv_loss_scale * sum_j G_j|| over all tensors and ranks
+ * (deterministic: fixed-order partials, rank-order combine), skips the whole step on the
+ * device if gn is not finite (w, m, v, params, stats untouched), and otherwise multiplies the
+ * reduced gradient by inv_loss_scale * min(1, max_grad_norm / (gn + 1e-6)) (the
+ * torch.nn.utils.clip_grad_norm_ rule) before the LAMB update.  Costs one extra read of the
+ * local bf16 grads at D = 1; at D > 1 (FUSED) the reduce-scatter moves into the extra pass,
+ * which writes the fp32 reduced shard that pass A then reads (4 * shard_size bytes allocated on
+ * first use).  Values are host settings used by subsequent steps. */
+typedef struct {
+    double grad_norm;   /* global norm of the unclipped, unscaled-by-clip gradient; NaN if disabled */
+    float clip;         /* applied clip coefficient (1 = none) */
+    int32_t skipped;    /* 1 if the step was skipped (non-finite gradient) */
+} lamb_step_info;
+/* EINVAL: max_grad_norm < 0 or NaN (0 disables clipping). */
+lamb_status lamb_set_grad_clip(lamb_t h, float max_grad_norm);
+/* EINVAL: inv_loss_scale not finite or <= 0 (1 disables unscaling). */
+lamb_status lamb_set_loss_scale(lamb_t h, float inv_loss_scale);
+/* Synchronises the device; reports the last step's pre-step outcome. */
+lamb_status lamb_get_step_info(lamb_t h, lamb_step_info* out);
+
 /* ---------------- checkpoint / resume with reshard (§4.4) ----------------
  * File format (little endian; one file per checkpoint, written by all ranks at disjoint
  * offsets): header {char magic[8] = "LAMBCKPT"; u32 version = 1; u32 world size that saved;

@@ -194,11 +194,32 @@ class OracleRun:
             G = G * self.D
         return reduce(G, f32(self.grad_scale))
 
-    def step(self, t: int) -> None:
+    def step(self, t: int, max_grad_norm: float = 0.0, inv_loss_scale: float = 1.0) -> dict:
+        """One LAMB step.  With the pre-step of SURVEY §8(f) NEXT #3 (reading Z12'):
+        g <- g * inv_loss_scale; gn = ||g|| over ALL tensors of the workload; skip the step
+        (state untouched) if gn is not finite; if max_grad_norm > 0 and
+        c = max_grad_norm / (gn + 1e-6) < 1, g <- c * g (torch clip_grad_norm_ rule)."""
+        info = {"grad_norm": None, "clip": 1.0, "skipped": False}
+        if max_grad_norm > 0.0 or inv_loss_scale != 1.0:
+            gsq = 0.0
+            for i in range(len(self.wl.tensors)):          # the GLOBAL norm needs every tensor
+                gsq += sumsq(self.grads(i, t) * f32(inv_loss_scale))
+            gn = float(np.sqrt(gsq))
+            info["grad_norm"] = gn
+            if not np.isfinite(gn):
+                info["skipped"] = True
+                return info
+            if max_grad_norm > 0.0:
+                c = f32(max_grad_norm) / (gn + 1e-6)
+                info["clip"] = min(1.0, c)
+        scale = f32(inv_loss_scale) * info["clip"]
         for i in self.ids:
             g = self.grads(i, t)
+            if scale != 1.0:
+                g = g * scale
             grp = self.groups[self.wl.tensors[i].group]
             self.stats[i] = lamb_tensor_step(self.w[i], self.m[i], self.v[i], g, grp, t)
+        return info
 
 
 def sharded_step(wl, pl: OraclePlan, w_flat: np.ndarray, m_flat: np.ndarray, v_flat: np.ndarray,

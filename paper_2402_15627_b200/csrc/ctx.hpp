@@ -74,6 +74,10 @@ struct lamb_ctx {
     std::vector<cudaEvent_t> tev;   // [max_steps][LAMB_N_PHASES + 1]
     int32_t t_max = 0, t_n = 0;
 
+    // pre-step (NEXT #3): global grad-norm clipping, loss-scale unscale, non-finite skip
+    float max_grad_norm = 0.f, inv_loss_scale = 1.f;
+    lamb::ClipState* d_clip = nullptr;
+    bool prestep() const { return max_grad_norm > 0.f || inv_loss_scale != 1.f; }
     // checkpoint (two-stage save: pinned staging + background writer thread)
     float* ck_stage = nullptr;          // pinned host, 3 x shard_size
     std::thread ck_thread;
@@ -82,8 +86,11 @@ struct lamb_ctx {
 
     uint64_t* flags(int j) const { return reinterpret_cast<uint64_t*>(peer_sync[j]); }
     uint64_t* epoch() const { return reinterpret_cast<uint64_t*>(sync + 8 * LAMB_MAX_RANKS); }
+    // sync buffer layout: [0,64) barrier flags, [64,72) epoch, [128,192) clip rows (double[8]),
+    // [256, ...) straddler exchange rows (double2[D][n_strad])
+    double* clip_rows(int j) const { return reinterpret_cast<double*>((j < 0 ? sync : peer_sync[j]) + 128); }
     double2* xbuf(int j) const {
-        return reinterpret_cast<double2*>((j < 0 ? sync : peer_sync[j]) + 128);
+        return reinterpret_cast<double2*>((j < 0 ? sync : peer_sync[j]) + 256);
     }
 };
 

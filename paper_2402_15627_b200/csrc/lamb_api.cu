@@ -138,7 +138,7 @@ static void free_ctx(lamb_ctx* h) {
     }
     void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->partials, h->segs, h->scale,
                     h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
-                    h->sync, h->g32, h->up32[0], h->up32[1], h->d_tensor_off, h->d_numel,
+                    h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_tensor_off, h->d_numel,
                     h->d_shard_base, h->d_bucket_base, h->d_bucket_slice};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -355,9 +355,11 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
     CUDA_STEP(cudaMemset(h->m, 0, (size_t)p.shard_size * 4));
     CUDA_STEP(cudaMemset(h->v, 0, (size_t)p.shard_size * 4));
     STEP(build_tables(h));
-    h->sync_bytes = 128 + sizeof(double2) * (size_t)D * std::max<size_t>(1, p.straddlers.size());
+    h->sync_bytes = 256 + sizeof(double2) * (size_t)D * std::max<size_t>(1, p.straddlers.size());
     CUDA_STEP(dalloc(&h->sync, h->sync_bytes));
     CUDA_STEP(cudaMemset(h->sync, 0, h->sync_bytes));
+    CUDA_STEP(dalloc(&h->d_clip, 1));
+    CUDA_STEP(cudaMemset(h->d_clip, 0, sizeof(lamb::ClipState)));
     CUDA_STEP(cudaHostAlloc(&h->err_flag_host, sizeof(int), cudaHostAllocMapped));
     *h->err_flag_host = 0;
     CUDA_STEP(cudaHostGetDevicePointer(&h->err_flag_dev, h->err_flag_host, 0));
@@ -462,6 +464,26 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     fp.n_local_strad = h->n_local_strad;
     fp.xbuf = h->xbuf(-1);
     memcpy(fp.groups, sp.groups, sizeof(sp.groups));
+    const bool pre = h->prestep();
+    lamb::ClipParams cp;
+    memset(&cp, 0, sizeof(cp));
+    if (pre) {
+        if (!h->g32 && D > 1) {   // FUSED + pre-step: the fp32 reduced shard lives here
+            CUDA_TRY(h, dalloc(&h->g32, (size_t)p.shard_size));
+        }
+        sp.clip = h->d_clip;
+        fp.clip = h->d_clip;
+        cp.partials = h->partials;
+        cp.n_items = h->n_items;
+        for (int j = 0; j < D; ++j) cp.rows[j] = h->clip_rows(fused ? j : -1);
+        cp.my_rows = h->clip_rows(-1);
+        cp.world = D;
+        cp.rank = r;
+        cp.grad_scale = h->cfg.grad_scale;
+        cp.inv_loss_scale = h->inv_loss_scale;
+        cp.max_grad_norm = h->max_grad_norm;
+        cp.out = h->d_clip;
+    }
 
     mark(h, 0, s);
     if (!nccl) {
@@ -472,7 +494,22 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         mark(h, 1, s);
         for (int j = 0; j < D; ++j)
             sp.gsrc[j] = fused ? h->peer_grad[j] : (grads ? (const __nv_bfloat16*)grads : h->grad);
-        LAUNCH(h, launch_pass_a(sp, D, false, h->grid_a, s));
+        if (pre) {
+            // pre-step: global ||g||^2 (FUSED: the reduce-scatter happens here, into g32)
+            sp.g32_out = h->g32;
+            LAUNCH(h, launch_grad_stats(sp, D, fused, h->grid_a, s));
+            LAUNCH(h, launch_clip_finalize(cp, s));
+            if (fused) {
+                LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+                LAUNCH(h, launch_clip_combine(cp, s));
+                sp.g32 = h->g32;
+                LAUNCH(h, launch_pass_a(sp, 0, true, h->grid_a, s));
+            } else {
+                LAUNCH(h, launch_pass_a(sp, D, false, h->grid_a, s));
+            }
+        } else {
+            LAUNCH(h, launch_pass_a(sp, D, false, h->grid_a, s));
+        }
         if (!fused) CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));   // D = 1: grads consumed
         mark(h, 2, s);
         for (int j = 0; j < D; ++j) fp.xrow[j] = h->xbuf(fused ? j : -1);
@@ -512,11 +549,22 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
                                       ncclSum, h->comm, h->comm_stream));
         CUDA_TRY(h, cudaEventRecord(h->ev_rs[b], h->comm_stream));
     }
-    for (int64_t b = 0; b < B; ++b) {
-        CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_rs[b], 0));
-        sp.item_begin = h->bucket_item_begin[b];
-        sp.item_end = h->bucket_item_begin[b + 1];
+    if (pre) {
+        // the global norm needs every bucket's reduced gradient: wait for all RS first
+        for (int64_t b = 0; b < B; ++b) CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_rs[b], 0));
+        LAUNCH(h, launch_grad_stats(sp, 0, false, h->grid_a, s));
+        LAUNCH(h, launch_clip_finalize(cp, s));
+        double* rows = h->clip_rows(-1);
+        NCCL_TRY(h, ncclAllGather(rows + r, rows, 1, ncclDouble, h->comm, s));
+        LAUNCH(h, launch_clip_combine(cp, s));
         LAUNCH(h, launch_pass_a(sp, 0, true, h->grid_a, s));
+    } else {
+        for (int64_t b = 0; b < B; ++b) {
+            CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_rs[b], 0));
+            sp.item_begin = h->bucket_item_begin[b];
+            sp.item_end = h->bucket_item_begin[b + 1];
+            LAUNCH(h, launch_pass_a(sp, 0, true, h->grid_a, s));
+        }
     }
     mark(h, 2, s);
     for (int j = 0; j < D; ++j) fp.xrow[j] = h->xbuf(-1);
@@ -683,6 +731,39 @@ extern "C" lamb_status lamb_set_lr(lamb_t h, int32_t group, float lr) {
     if (group < 0 || group >= (int32_t)h->groups.size()) return fail(h, LAMB_EINVAL, "group out of range");
     if (!(lr >= 0.f)) return fail(h, LAMB_EINVAL, "lr must be >= 0");
     h->groups[group].lr = lr;
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_set_grad_clip(lamb_t h, float max_grad_norm) {
+    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
+    if (!(max_grad_norm >= 0.f)) return fail(h, LAMB_EINVAL, "max_grad_norm must be >= 0");
+    h->max_grad_norm = max_grad_norm;
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_set_loss_scale(lamb_t h, float inv_loss_scale) {
+    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
+    if (!(inv_loss_scale > 0.f) || !std::isfinite(inv_loss_scale))
+        return fail(h, LAMB_EINVAL, "inv_loss_scale must be finite and > 0");
+    h->inv_loss_scale = inv_loss_scale;
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_get_step_info(lamb_t h, lamb_step_info* out) {
+    if (!h || !out) return fail(h, LAMB_EINVAL, "null argument");
+    cudaSetDevice(h->device);
+    CUDA_TRY(h, cudaDeviceSynchronize());
+    lamb::ClipState cs;
+    CUDA_TRY(h, cudaMemcpy(&cs, h->d_clip, sizeof(cs), cudaMemcpyDeviceToHost));
+    if (!h->prestep()) {
+        out->grad_norm = NAN;
+        out->clip = 1.f;
+        out->skipped = 0;
+        return LAMB_OK;
+    }
+    out->grad_norm = cs.grad_norm;
+    out->clip = cs.clip;
+    out->skipped = cs.skip;
     return LAMB_OK;
 }
 

@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_a_kernel(const __grid_con
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
-    const float gs = P.grad_scale;
+    if (P.clip && P.clip->skip) return;
+    const float gs = P.clip ? P.clip->gs : P.grad_scale;
     for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
         const Item I = P.items[it];
         const GroupConst& G = P.groups[I.group];
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_b_kernel(const __grid_con
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
+    if (P.clip && P.clip->skip) return;
     for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
         const Item I = P.items[it];
         const GroupConst& G = P.groups[I.group];
@@ -225,6 +227,100 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_b_kernel(const __grid_con
     if constexpr (ND > 1) __threadfence_system();   // peer stores visible before the barrier
 }
 
+// ------------------------------------------------------------ pre-step (NEXT #3)
+// Sum of squares of the reduced gradient sums per item (fp32 block partials -> fp64, as the
+// norms), optionally materialising the fp32 sums into g32_out (FUSED, D > 1: the reduce-scatter
+// happens here once and pass A reads the local fp32 shard instead of pulling again).
+template <int NS, bool MAT>
+__global__ void __launch_bounds__(kThreads) grad_stats_kernel(const __grid_constant__ StepParams P) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
+    constexpr int U = 4;
+    for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
+        const Item I = P.items[it];
+        const int n = I.n_chunk;
+        float4* __restrict__ gout = reinterpret_cast<float4*>(P.g32_out + I.shard_off);
+        double acc = 0.0;
+        int c = lane;
+        for (; c + 32 * (U - 1) < n; c += 32 * U) {
+            float4 g[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) g[k] = load_grad<NS>(P, I, 4 * (int64_t)(c + 32 * k));
+            float s = 0.f;
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                if constexpr (MAT) __stcs(gout + c + 32 * k, g[k]);
+                s = __fmaf_rn(g[k].x, g[k].x, s);
+                s = __fmaf_rn(g[k].y, g[k].y, s);
+                s = __fmaf_rn(g[k].z, g[k].z, s);
+                s = __fmaf_rn(g[k].w, g[k].w, s);
+            }
+            acc += (double)s;
+        }
+        for (; c < n; c += 32) {
+            const float4 g = load_grad<NS>(P, I, 4 * (int64_t)c);
+            if constexpr (MAT) __stcs(gout + c, g);
+            float s = __fmaf_rn(g.x, g.x, 0.f);
+            s = __fmaf_rn(g.y, g.y, s);
+            s = __fmaf_rn(g.z, g.z, s);
+            s = __fmaf_rn(g.w, g.w, s);
+            acc += (double)s;
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) P.partials[it] = make_double2(acc, 0.0);
+    }
+    if constexpr (MAT) __threadfence();
+}
+
+__device__ __forceinline__ void clip_state(double total, const ClipParams& P) {
+    const double sc = (double)P.grad_scale * (double)P.inv_loss_scale;
+    const double gn = sqrt(total) * fabs(sc);
+    ClipState cs;
+    cs.grad_norm = gn;
+    cs.skip = isfinite(gn) ? 0 : 1;
+    double c = 1.0;
+    if (P.max_grad_norm > 0.f && !cs.skip) {
+        const double cc = (double)P.max_grad_norm / (gn + 1e-6);   // torch clip_grad_norm_ rule
+        if (cc < 1.0) c = cc;
+    }
+    cs.clip = (float)c;
+    cs.gs = (float)(sc * c);
+    cs.pad = 0;
+    *P.out = cs;
+}
+
+// One CTA: fixed-order sum of all item partials of this rank; D = 1 -> clip state, else the
+// rank's row is stored into every rank's row buffer (slot `rank`).
+constexpr int kClipThreads = 1024;
+__global__ void __launch_bounds__(kClipThreads) clip_finalize_kernel(const __grid_constant__ ClipParams P) {
+    __shared__ double red[kClipThreads];
+    const int tid = threadIdx.x;
+    double s = 0.0;
+    for (int64_t i = tid; i < P.n_items; i += kClipThreads) s += P.partials[i].x;
+    red[tid] = s;
+    __syncthreads();
+    for (int o = kClipThreads / 2; o > 0; o >>= 1) {
+        if (tid < o) red[tid] += red[tid + o];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        if (P.world == 1) {
+            clip_state(red[0], P);
+        } else {
+            for (int j = 0; j < P.world; ++j) P.rows[j][P.rank] = red[0];
+            __threadfence_system();
+        }
+    }
+}
+
+// After the rows arrived (barrier / all-gather): total in rank order -> clip state.
+__global__ void clip_combine_kernel(const __grid_constant__ ClipParams P) {
+    double t = 0.0;
+    for (int j = 0; j < P.world; ++j) t += P.my_rows[j];
+    clip_state(t, P);
+}
+
 // ------------------------------------------------------------ finalize
 __device__ __forceinline__ void trust_ratio(double w2, double u2, const GroupConst& G, int tensor,
                                             const FinalizeParams& P) {
@@ -242,6 +338,7 @@ constexpr int kFinThreads = 256;
 __global__ void __launch_bounds__(kFinThreads) finalize_segments_kernel(const __grid_constant__ FinalizeParams P) {
     __shared__ double2 red[kFinThreads];
     const int tid = threadIdx.x;
+    if (P.clip && P.clip->skip) return;
     const SegDesc S = P.segs[blockIdx.x];
     double w2 = 0.0, u2 = 0.0;
     int64_t i = S.item_begin + tid;
@@ -287,7 +384,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_segments_kernel(const __
 // One thread per straddler this rank touches: sum the D rows in rank order.
 __global__ void finalize_straddlers_kernel(const __grid_constant__ FinalizeParams P) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= P.n_local_strad) return;
+    if (k >= P.n_local_strad || (P.clip && P.clip->skip)) return;
     const int slot = P.strad_slots[k];
     double w2 = 0.0, u2 = 0.0;
     for (int j = 0; j < P.world; ++j) {
@@ -465,6 +562,38 @@ int pass_grid(int device, int nsrc, bool g32, bool pass_b, int ndst) {
     };
     if (pass_b) return ndst <= 1 ? pick_b(std::integral_constant<int, 1>()) : pick_b(std::integral_constant<int, 8>());
     return nsrc <= 1 ? pick_a(std::integral_constant<int, 1>()) : pick_a(std::integral_constant<int, 8>());
+}
+
+template <int NS, bool MAT>
+static cudaError_t grad_stats_v(const StepParams& p, int grid, cudaStream_t s) {
+    grad_stats_kernel<NS, MAT><<<grid, kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grad_stats(const StepParams& p, int nsrc, bool mat, int grid, cudaStream_t s) {
+    if (p.item_end <= p.item_begin) return cudaSuccess;
+    switch (nsrc) {
+        case 0: return grad_stats_v<0, false>(p, grid, s);
+        case 1: return grad_stats_v<1, false>(p, grid, s);
+        case 2: return mat ? grad_stats_v<2, true>(p, grid, s) : grad_stats_v<2, false>(p, grid, s);
+        case 3: return mat ? grad_stats_v<3, true>(p, grid, s) : grad_stats_v<3, false>(p, grid, s);
+        case 4: return mat ? grad_stats_v<4, true>(p, grid, s) : grad_stats_v<4, false>(p, grid, s);
+        case 5: return mat ? grad_stats_v<5, true>(p, grid, s) : grad_stats_v<5, false>(p, grid, s);
+        case 6: return mat ? grad_stats_v<6, true>(p, grid, s) : grad_stats_v<6, false>(p, grid, s);
+        case 7: return mat ? grad_stats_v<7, true>(p, grid, s) : grad_stats_v<7, false>(p, grid, s);
+        case 8: return mat ? grad_stats_v<8, true>(p, grid, s) : grad_stats_v<8, false>(p, grid, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_clip_finalize(const ClipParams& p, cudaStream_t s) {
+    clip_finalize_kernel<<<1, kClipThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_clip_combine(const ClipParams& p, cudaStream_t s) {
+    clip_combine_kernel<<<1, 1, 0, s>>>(p);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_finalize_segments(const FinalizeParams& p, cudaStream_t s) {

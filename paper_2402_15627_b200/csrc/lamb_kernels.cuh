@@ -42,6 +42,27 @@ struct GroupConst {
     int32_t adapt;
 };
 
+// Pre-step state, written on the device by clip_combine_kernel:
+// gs = grad_scale * inv_loss_scale * clip (fp32, what pass A multiplies the reduced sum by),
+// skip = 1 when the global gradient norm is not finite (the whole step is a no-op).
+struct ClipState {
+    double grad_norm;
+    float gs;
+    float clip;
+    int32_t skip;
+    int32_t pad;
+};
+
+struct ClipParams {
+    const double2* partials;        // [n_items] .x = sum of squares of the item's reduced grads
+    int64_t n_items;
+    double* rows[LAMB_MAX_RANKS];   // rank j's clip row buffer (double[D]); this rank writes slot `rank`
+    const double* my_rows;          // this rank's row buffer
+    int32_t world, rank;
+    float grad_scale, inv_loss_scale, max_grad_norm;
+    ClipState* out;
+};
+
 struct StepParams {
     const Item* items;
     int64_t item_begin, item_end;
@@ -55,6 +76,8 @@ struct StepParams {
     float* v;
     double2* partials;        // [n_items] (sum w^2, sum u^2)
     const float* scale;       // [T] lr * ratio (pass B)
+    const ClipState* clip;    // non-null: pre-step enabled (gs from device, skip flag)
+    float* g32_out;           // grad_stats: materialise the fp32 reduced sums here (FUSED + clip)
     __nv_bfloat16* pdst[LAMB_MAX_RANKS];   // param buffers pass B stores into
     GroupConst groups[LAMB_MAX_GROUPS];
 };
@@ -78,12 +101,16 @@ struct FinalizeParams {
     const int32_t* strad_group;     // [n_local_strad]
     int32_t n_local_strad;
     const double2* xbuf;            // this rank's exchange buffer
+    const ClipState* clip;          // skip flag (pre-step)
     GroupConst groups[LAMB_MAX_GROUPS];
 };
 
 // Host launchers (lamb_kernels.cu).  `occ_grid` = persistent grid size.
 cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int grid, cudaStream_t s);
 cudaError_t launch_pass_b(const StepParams& p, int ndst, int grid, cudaStream_t s);
+cudaError_t launch_grad_stats(const StepParams& p, int nsrc, bool materialise, int grid, cudaStream_t s);
+cudaError_t launch_clip_finalize(const ClipParams& p, cudaStream_t s);
+cudaError_t launch_clip_combine(const ClipParams& p, cudaStream_t s);
 cudaError_t launch_finalize_segments(const FinalizeParams& p, cudaStream_t s);
 cudaError_t launch_finalize_straddlers(const FinalizeParams& p, cudaStream_t s);
 cudaError_t launch_barrier(uint64_t* const* flags, uint64_t* epoch, int rank, int world,

@@ -63,6 +63,10 @@ class lamb_plan_view(ctypes.Structure):
                 ("segments", _P64), ("straddlers", _P64)]
 
 
+class lamb_step_info(ctypes.Structure):
+    _fields_ = [("grad_norm", ctypes.c_double), ("clip", ctypes.c_float), ("skipped", ctypes.c_int32)]
+
+
 class lamb_synth_tensor(ctypes.Structure):
     _fields_ = [("init", ctypes.c_int32), ("gexp", ctypes.c_int32)]
 
@@ -87,6 +91,9 @@ _SIGS = {
     "lamb_get_state": (_st, [_vp, ctypes.c_int32, _vp, ctypes.c_int32, _vp]),
     "lamb_get_tensor_stats": (_st, [_vp, _vp, _vp, _vp]),
     "lamb_set_lr": (_st, [_vp, ctypes.c_int32, ctypes.c_float]),
+    "lamb_set_grad_clip": (_st, [_vp, ctypes.c_float]),
+    "lamb_set_loss_scale": (_st, [_vp, ctypes.c_float]),
+    "lamb_get_step_info": (_st, [_vp, ctypes.POINTER(lamb_step_info)]),
     "lamb_checkpoint_save": (_st, [_vp, ctypes.c_char_p, ctypes.c_int64, _vp]),
     "lamb_checkpoint_wait": (_st, [_vp]),
     "lamb_checkpoint_load": (_st, [_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), _vp]),
@@ -283,6 +290,18 @@ class Lamb:
 
     def set_lr(self, group: int, lr: float) -> None:
         check(lamb_set_lr(self.h, group, lr), self.h)
+
+    # -- pre-step: clipping / loss scale / non-finite skip
+    def set_grad_clip(self, max_grad_norm: float) -> None:
+        check(lamb_set_grad_clip(self.h, max_grad_norm), self.h)
+
+    def set_loss_scale(self, inv_loss_scale: float) -> None:
+        check(lamb_set_loss_scale(self.h, inv_loss_scale), self.h)
+
+    def step_info(self) -> dict:
+        i = lamb_step_info()
+        check(lamb_get_step_info(self.h, ctypes.byref(i)), self.h)
+        return {"grad_norm": i.grad_norm, "clip": i.clip, "skipped": bool(i.skipped)}
 
     # -- checkpoint / resume (two-stage save, reshard on load)
     def checkpoint_save(self, path: str, step: int, stream=None) -> None:

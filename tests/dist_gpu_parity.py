@@ -74,6 +74,42 @@ def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, chec
               f"max rel err w={worst:.2e}", flush=True)
 
 
+def clip_case(world, rank, local, mode):
+    """Pre-step at D ranks: the global norm spans every rank's shard; clipping active; then a
+    non-finite gradient on one rank makes every rank skip."""
+    from paper_2402_15627_b200 import lamb
+    rng = np.random.default_rng(99)
+    tensors = W.random_table(rng, 40, max_numel=5000, p_big=0.2, big=40_000)
+    wl = W.Workload("clipd", 72, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+    gn1 = np.sqrt(sum(np.sum(orc.grads(i, 1) ** 2) for i in orc.ids))
+    max_norm = float(np.float32(0.3 * gn1))
+    L = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
+                  device=local, comm_mode=mode, bucket_cap=8192, pg=dist.group.WORLD)
+    L.synth_init(spec, wl.seed)
+    L.set_grad_clip(max_norm)
+    for t in (1, 2):
+        L.synth_grads(spec, wl.seed, rank + 1, t)
+        L.step(t)
+        info = orc.step(t, max_grad_norm=max_norm)
+        gi = L.step_info()
+        assert abs(gi["grad_norm"] - info["grad_norm"]) <= 1e-6 * info["grad_norm"], (gi, info)
+        assert abs(gi["clip"] - info["clip"]) <= 1e-6 and info["clip"] < 1 and not gi["skipped"]
+    compare_state(L, orc, 2, check_params=False)
+    w_before = L.get_state(2).copy()
+    L.synth_grads(spec, wl.seed, rank + 1, 3)
+    if rank == world - 1:
+        L.grad_buffer()[7] = float("nan")
+    L.step(3)
+    assert L.step_info()["skipped"]
+    assert np.array_equal(w_before.view(np.uint32), L.get_state(2).view(np.uint32))
+    L.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] clip D={world} mode={mode} (global norm, clip, skip on NaN)", flush=True)
+
+
 def ckpt_case(world, rank, local, mode):
     """Checkpoint saved by D ranks; reloaded (a) by D ranks with another bucket cap and
     (b) by rank 0 alone at D = 1 (reshard); both continue and must match the oracle."""
@@ -143,6 +179,7 @@ def main():
     run_case("stress", W.Workload("stress", 51, stress, W.default_groups()), world, rank, local, mode, 2,
              cap=100_000)
     ckpt_case(world, rank, local, mode)
+    clip_case(world, rank, local, mode)
     if a.big:
         wl = W.gpt_1p3b()
         ids = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 289, 290]

@@ -273,3 +273,61 @@ def test_checkpoint_resume_and_reshard(lamb, tmp_path):
         C = lamb.Lamb([(10, 0)], wl.groups)
         C.checkpoint_load(path)
     A.close()
+
+
+@pytest.mark.parametrize("frac,inv_scale", [(0.25, 1.0), (10.0, 1.0), (0.5, 2.0 ** -10)])
+def test_prestep_clip_and_loss_scale(lamb, frac, inv_scale):
+    """NEXT #3 on the GPU: global grad-norm clipping (clip active / inactive) and loss-scale
+    unscaling against the oracle's pre-step; reported norm and clip coefficient match."""
+    rng = np.random.default_rng(31)
+    tensors = W.random_table(rng, 30, max_numel=6000, p_big=0.2, big=40_000)
+    wl = W.Workload("clip", 90, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    S = 1.0 / inv_scale
+    orc = oracle.OracleRun(wl)
+    gn1 = np.sqrt(sum(np.sum(orc.grads(i, 1) ** 2) for i in orc.ids))
+    max_norm = float(np.float32(frac * gn1))
+    if S != 1.0:   # feed loss-scaled grads S * g (exact in bf16 for a power of two)
+        orig = orc.grads
+        orc.grads = lambda i, t: orig(i, t) * S
+    L = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=20_000)
+    L.synth_init(spec, wl.seed)
+    L.set_grad_clip(max_norm)
+    L.set_loss_scale(inv_scale)
+    for t in (1, 2, 3):
+        L.synth_grads(spec, wl.seed, 1, t)
+        if S != 1.0:
+            g = L.grad_buffer()
+            g.copy_((g.float() * S).bfloat16())
+        L.step(t)
+        info = orc.step(t, max_grad_norm=max_norm, inv_loss_scale=inv_scale)
+        gi = L.step_info()
+        assert not gi["skipped"]
+        assert gi["grad_norm"] == pytest.approx(info["grad_norm"], rel=1e-6)
+        assert gi["clip"] == pytest.approx(info["clip"], rel=1e-6)
+        if frac < 1:
+            assert info["clip"] < 1.0
+    compare_state(L, orc, 3)
+    L.close()
+
+
+def test_prestep_nonfinite_skip(lamb):
+    wl = W.toy()
+    spec = spec_of(wl)
+    L = run_gpu(wl, steps=1)
+    L.set_grad_clip(1.0)
+    before = [L.get_state(k).copy() for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V)]
+    p0 = L.param_buffer().clone()
+    L.synth_grads(spec, wl.seed, 1, 2)
+    L.grad_buffer()[100] = float("inf")
+    L.step(2)
+    info = L.step_info()
+    assert info["skipped"]
+    after = [L.get_state(k) for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V)]
+    for a, b in zip(before, after):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert torch.equal(p0.view(torch.int16), L.param_buffer().view(torch.int16))
+    L.synth_grads(spec, wl.seed, 1, 2)     # next step with finite grads proceeds
+    L.step(2)
+    assert not L.step_info()["skipped"]
+    L.close()
