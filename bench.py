@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="gpt1.3b", choices=list(W.CONFIGS))
     ap.add_argument("--comm", default="fused", choices=["fused", "nccl"])
+    ap.add_argument("--clip", type=float, default=0.0,
+                    help="enable the NEXT #3 pre-step with this max grad norm (0 = off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
@@ -184,6 +186,8 @@ def main():
                   device=local, comm_mode=comm, bucket_cap=wl.cap, timing=True, pg=pg)
     L.synth_init(spec, wl.seed)
     L.synth_grads(spec, wl.seed, rank + 1, 1)      # PER_RANK gradients, resident in HBM
+    if args.clip > 0:
+        L.set_grad_clip(args.clip)
     stream = torch.cuda.current_stream()
     K, Wm = args.steps, args.warmup
 
@@ -289,6 +293,7 @@ def main():
             "config": {"workload": wl.name, "n_params": wl.n_params, "n_tensors": len(wl.tensors),
                        "flat_size": L.plan.flat_size, "world_size": world,
                        "comm": args.comm if world > 1 else "none", "bucket_cap": wl.cap,
+                       "prestep_clip": args.clip if args.clip > 0 else None,
                        "l2": "inputs larger than L2 (fp32 state of the shard >> 126 MB)",
                        "parallelism": f"zero2-dp{world}"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
