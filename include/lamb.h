@@ -140,6 +140,24 @@ lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void* stream);
 lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_params,
                            int64_t step, void* stream);
 
+/* ---------------- per-bucket stepping: overlap with backward/forward --------
+ * PAPER.md §3.2: the reduce-scatter of a model chunk starts right after its
+ * backward, the all-gather right before its forward (prefetched for the first chunk).  Every
+ * tensor lives in exactly one bucket, so the complete LAMB update of a bucket (RS, moments,
+ * segmented norms incl. straddlers, trust ratio, apply, cast) can run as soon as that bucket's
+ * gradients are final, overlapped with the backward of the remaining buckets. */
+#define LAMB_BUCKET_DEFER_AG 1   /* pass B writes only this rank's slices; gather later */
+/* COLLECTIVE (all ranks, same bucket order), asynchronous on `stream`: the LAMB step of
+ * bucket `bucket` (0 <= bucket < n_buckets).  Without LAMB_BUCKET_DEFER_AG the bucket's params
+ * are all-gathered at the end (as lamb_step); with it, call lamb_gather_bucket before the
+ * bucket's next forward.  Calling it for every bucket once equals one lamb_step.
+ * EINVAL: bucket out of range, step < 1, unknown flags.  ESTATE: master not set.
+ * EUNSUPPORTED: the pre-step is enabled (its global norm needs the whole table). */
+lamb_status lamb_step_bucket(lamb_t h, int64_t bucket, int64_t step, int32_t flags, void* stream);
+/* Deferred all-gather of one bucket's bf16 params (FUSED: NVLink pull of the D-1 peer slices;
+ * NCCL: ncclAllGather, COLLECTIVE).  No-op at D = 1. */
+lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream);
+
 /* COLLECTIVE (barrier-free teardown of this rank's peer mappings and communicator). */
 void lamb_destroy(lamb_t h);
 

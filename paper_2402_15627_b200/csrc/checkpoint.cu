@@ -18,6 +18,8 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
+#include <atomic>
 #include <cstring>
 
 #include "ctx.hpp"
@@ -58,6 +60,56 @@ bool pread_all(int fd, void* buf, size_t n, off_t off) {
         off += k;
     }
     return true;
+}
+
+// File I/O of one rank's segments: split into <= 64 MiB pieces, served by a pool of host
+// threads (pread/pwrite at disjoint offsets are thread-safe).
+struct IoTask {
+    float* host;
+    off_t off;
+    size_t bytes;
+};
+
+std::vector<IoTask> segment_tasks(const Plan& p, float* stage, const std::vector<int64_t>& cum, int64_t doff) {
+    const int64_t N = cum.back();
+    const size_t sh = (size_t)p.shard_size;
+    const size_t piece = 64u << 20;
+    std::vector<IoTask> tasks;
+    for (int64_t k = 0; k < p.n_segments(); ++k) {
+        const int64_t t = p.segments[4 * k], soff = p.segments[4 * k + 1];
+        const int64_t toff = p.segments[4 * k + 2], len = p.segments[4 * k + 3];
+        for (int x = 0; x < 3; ++x) {
+            float* h = stage + x * sh + soff;
+            off_t off = doff + ((int64_t)x * N + cum[t] + toff) * 4;
+            size_t left = (size_t)len * 4;
+            while (left > 0) {
+                const size_t n = left < piece ? left : piece;
+                tasks.push_back({h, off, n});
+                h += n / 4;
+                off += (off_t)n;
+                left -= n;
+            }
+        }
+    }
+    return tasks;
+}
+
+bool run_io(int fd, const std::vector<IoTask>& tasks, bool write) {
+    const int nthreads = (int)std::min<size_t>(8, std::max<size_t>(1, tasks.size()));
+    std::atomic<size_t> next{0};
+    std::atomic<bool> ok{true};
+    auto worker = [&]() {
+        for (size_t i = next++; i < tasks.size() && ok; i = next++) {
+            const IoTask& T = tasks[i];
+            const bool r = write ? pwrite_all(fd, T.host, T.bytes, T.off) : pread_all(fd, T.host, T.bytes, T.off);
+            if (!r) ok = false;
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int i = 1; i < nthreads; ++i) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    return ok;
 }
 
 std::vector<int64_t> prefix(const Plan& p) {
@@ -130,17 +182,9 @@ extern "C" lamb_status lamb_checkpoint_save(lamb_t h, const char* path, int64_t 
                 return fail_io("header");
             }
         }
-        const size_t sh = (size_t)p.shard_size;
-        for (int64_t k = 0; k < p.n_segments(); ++k) {
-            const int64_t t = p.segments[4 * k], soff = p.segments[4 * k + 1];
-            const int64_t toff = p.segments[4 * k + 2], len = p.segments[4 * k + 3];
-            for (int x = 0; x < 3; ++x) {
-                const off_t off = doff + ((int64_t)x * N + cum[t] + toff) * 4;
-                if (!pwrite_all(fd, h->ck_stage + x * sh + soff, (size_t)len * 4, off)) {
-                    close(fd);
-                    return fail_io("write");
-                }
-            }
+        if (!run_io(fd, segment_tasks(p, h->ck_stage, cum, doff), true)) {
+            close(fd);
+            return fail_io("write");
         }
         if (fdatasync(fd) != 0) {
             close(fd);
@@ -177,13 +221,7 @@ extern "C" lamb_status lamb_checkpoint_load(lamb_t h, const char* path, int64_t*
     }
     const size_t sh = (size_t)p.shard_size;
     memset(h->ck_stage, 0, 3 * sh * sizeof(float));   // padding stays exactly zero
-    for (int64_t k = 0; k < p.n_segments() && ok; ++k) {
-        const int64_t t = p.segments[4 * k], soff = p.segments[4 * k + 1];
-        const int64_t toff = p.segments[4 * k + 2], len = p.segments[4 * k + 3];
-        for (int x = 0; x < 3 && ok; ++x)
-            ok = pread_all(fd, h->ck_stage + x * sh + soff, (size_t)len * 4,
-                           H.data_off + ((int64_t)x * N + cum[t] + toff) * 4);
-    }
+    ok = run_io(fd, segment_tasks(p, h->ck_stage, cum, H.data_off), false);
     close(fd);
     if (!ok) return lamb_fail(h, LAMB_EINVAL, std::string("checkpoint load: short read of ") + path);
     cudaSetDevice(h->device);

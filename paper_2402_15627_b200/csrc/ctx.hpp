@@ -38,6 +38,9 @@ struct lamb_ctx {
     Item* items = nullptr;
     int64_t n_items = 0;
     std::vector<int64_t> bucket_item_begin;   // [B+1] items of bucket b: [b], [b+1)
+    std::vector<int64_t> bucket_seg_begin;    // [B+1] this rank's segments of bucket b
+    std::vector<int64_t> bucket_strad_begin;  // [B+1] this rank's local straddler slots of bucket b
+    std::vector<uint8_t> bucket_has_strad;    // [B] bucket holds a straddler (same on all ranks)
     double2* partials = nullptr;
     SegDesc* segs = nullptr;
     float* scale = nullptr;
@@ -77,6 +80,7 @@ struct lamb_ctx {
     // pre-step (NEXT #3): global grad-norm clipping, loss-scale unscale, non-finite skip
     float max_grad_norm = 0.f, inv_loss_scale = 1.f;
     lamb::ClipState* d_clip = nullptr;
+    double* d_clip_blocks = nullptr;
     bool prestep() const { return max_grad_norm > 0.f || inv_loss_scale != 1.f; }
     // checkpoint (two-stage save: pinned staging + background writer thread)
     float* ck_stage = nullptr;          // pinned host, 3 x shard_size

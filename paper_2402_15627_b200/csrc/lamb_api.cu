@@ -138,7 +138,7 @@ static void free_ctx(lamb_ctx* h) {
     }
     void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->partials, h->segs, h->scale,
                     h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
-                    h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_tensor_off, h->d_numel,
+                    h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_clip_blocks, h->d_tensor_off, h->d_numel,
                     h->d_shard_base, h->d_bucket_base, h->d_bucket_slice};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -163,12 +163,21 @@ static lamb_status build_tables(lamb_ctx* h) {
     std::vector<int32_t> ls_slot, ls_tensor, ls_group;
     const int64_t B = p.n_buckets();
     h->bucket_item_begin.assign(B + 1, 0);
+    h->bucket_seg_begin.assign(B + 1, 0);
+    h->bucket_strad_begin.assign(B + 1, 0);
+    h->bucket_has_strad.assign(B, 0);
+    for (int64_t t : p.straddlers) h->bucket_has_strad[p.tensor_bucket[t]] = 1;
     int64_t b = 0;
     for (int64_t s = 0; s < nseg; ++s) {
         const int64_t t = p.segments[4 * s], soff = p.segments[4 * s + 1];
         const int64_t len = p.segments[4 * s + 3];
         const int64_t tb = p.tensor_bucket[t];
-        while (b < tb) h->bucket_item_begin[++b] = (int64_t)items.size();
+        while (b < tb) {
+            ++b;
+            h->bucket_item_begin[b] = (int64_t)items.size();
+            h->bucket_seg_begin[b] = s;
+            h->bucket_strad_begin[b] = (int64_t)ls_slot.size();
+        }
         const int64_t slice = p.buckets[4 * tb + 1] / p.world;
         const int64_t flat0 = p.buckets[4 * tb] + (int64_t)p.rank * slice + (soff - p.shard_base[tb]);
         // the segment rounded up to 8 stays inside zero padding (P2: next start is 8-aligned,
@@ -197,7 +206,12 @@ static lamb_status build_tables(lamb_ctx* h) {
             ls_group.push_back(p.group[t]);
         }
     }
-    while (b < B) h->bucket_item_begin[++b] = (int64_t)items.size();
+    while (b < B) {
+        ++b;
+        h->bucket_item_begin[b] = (int64_t)items.size();
+        h->bucket_seg_begin[b] = nseg;
+        h->bucket_strad_begin[b] = (int64_t)ls_slot.size();
+    }
     h->n_items = (int64_t)items.size();
     h->n_local_strad = (int32_t)ls_slot.size();
     CUDA_TRY(h, upload(&h->items, items));
@@ -359,6 +373,7 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
     CUDA_STEP(dalloc(&h->sync, h->sync_bytes));
     CUDA_STEP(cudaMemset(h->sync, 0, h->sync_bytes));
     CUDA_STEP(dalloc(&h->d_clip, 1));
+    CUDA_STEP(dalloc(&h->d_clip_blocks, lamb::kClipBlocksMax));
     CUDA_STEP(cudaMemset(h->d_clip, 0, sizeof(lamb::ClipState)));
     CUDA_STEP(cudaHostAlloc(&h->err_flag_host, sizeof(int), cudaHostAllocMapped));
     *h->err_flag_host = 0;
@@ -428,17 +443,25 @@ static inline void mark(lamb_ctx* h, int phase, cudaStream_t s) {
         ++(h)->launches;                                                                      \
     } while (0)
 
-static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStream_t s) {
+// One LAMB step over the buckets [b0, b1) (the whole table for lamb_step, one bucket for
+// lamb_step_bucket).  Every tensor lives in exactly one bucket, so a bucket range is a
+// self-contained LAMB update; only the pre-step's global norm needs the whole table.
+// defer_ag: pass B writes only this rank's slices; the all-gather is lamb_gather_bucket.
+static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStream_t s, int64_t b0,
+                             int64_t b1, bool defer_ag) {
     const Plan& p = h->plan;
     const int D = h->cfg.world_size, r = h->cfg.rank;
     const bool fused = D > 1 && h->cfg.comm_mode == LAMB_COMM_FUSED;
     const bool nccl = D > 1 && h->cfg.comm_mode == LAMB_COMM_NCCL;
+    const bool whole = b0 == 0 && b1 == p.n_buckets();
+    bool strad = false;   // a bucket in range holds a straddler (identical on every rank)
+    for (int64_t b = b0; b < b1; ++b) strad = strad || h->bucket_has_strad[b];
 
     StepParams sp;
     memset(&sp, 0, sizeof(sp));
     sp.items = h->items;
-    sp.item_begin = 0;
-    sp.item_end = h->n_items;
+    sp.item_begin = h->bucket_item_begin[b0];
+    sp.item_end = h->bucket_item_begin[b1];
     sp.grad_scale = h->cfg.grad_scale;
     sp.w = h->w;
     sp.m = h->m;
@@ -448,8 +471,8 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     group_consts(h, t, sp.groups);
     FinalizeParams fp;
     memset(&fp, 0, sizeof(fp));
-    fp.segs = h->segs;
-    fp.n_segs = p.n_segments();
+    fp.segs = h->segs + h->bucket_seg_begin[b0];
+    fp.n_segs = h->bucket_seg_begin[b1] - h->bucket_seg_begin[b0];
     fp.partials = h->partials;
     fp.scale = h->scale;
     fp.w_sq = h->w_sq;
@@ -458,16 +481,17 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     fp.world = D;
     fp.rank = r;
     fp.n_strad = (int32_t)p.straddlers.size();
-    fp.strad_slots = h->strad_slots;
-    fp.strad_tensor = h->strad_tensor;
-    fp.strad_group = h->strad_group;
-    fp.n_local_strad = h->n_local_strad;
+    fp.strad_slots = h->strad_slots + h->bucket_strad_begin[b0];
+    fp.strad_tensor = h->strad_tensor + h->bucket_strad_begin[b0];
+    fp.strad_group = h->strad_group + h->bucket_strad_begin[b0];
+    fp.n_local_strad = (int32_t)(h->bucket_strad_begin[b1] - h->bucket_strad_begin[b0]);
     fp.xbuf = h->xbuf(-1);
     memcpy(fp.groups, sp.groups, sizeof(sp.groups));
     const bool pre = h->prestep();
     lamb::ClipParams cp;
     memset(&cp, 0, sizeof(cp));
     if (pre) {
+        if (!whole) return fail(h, LAMB_EUNSUPPORTED, "the pre-step (clip / loss scale) needs the whole table: use lamb_step");
         if (!h->g32 && D > 1) {   // FUSED + pre-step: the fp32 reduced shard lives here
             CUDA_TRY(h, dalloc(&h->g32, (size_t)p.shard_size));
         }
@@ -483,6 +507,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         cp.inv_loss_scale = h->inv_loss_scale;
         cp.max_grad_norm = h->max_grad_norm;
         cp.out = h->d_clip;
+        cp.block_sums = h->d_clip_blocks;
     }
 
     mark(h, 0, s);
@@ -515,17 +540,19 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         for (int j = 0; j < D; ++j) fp.xrow[j] = h->xbuf(fused ? j : -1);
         LAUNCH(h, launch_finalize_segments(fp, s));
         mark(h, 3, s);
-        if (fused) {
+        if (fused && strad) {
+            // straddler rows travel through peer memory: barrier, then sum in rank order
             LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
-            if (h->n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
+            if (fp.n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
         }
         mark(h, 4, s);
-        for (int j = 0; j < D; ++j) sp.pdst[j] = fused ? h->peer_param[j] : h->param;
-        LAUNCH(h, launch_pass_b(sp, fused ? D : 1, h->grid_b, s));
+        const bool push = fused && !defer_ag;
+        for (int j = 0; j < D; ++j) sp.pdst[j] = push ? h->peer_param[j] : h->param;
+        LAUNCH(h, launch_pass_b(sp, push ? D : 1, h->grid_b, s));
         mark(h, 5, s);
         if (fused) {
+            // params complete everywhere, and every rank finished reading this rank's grads
             LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
-            // every rank finished pass A (peer reads of this rank's grads) before this barrier
             CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));
         }
         mark(h, 6, s);
@@ -533,17 +560,16 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     }
 
     // ---------------- NCCL baseline, per-bucket pipeline on (s, comm_stream)
-    const int64_t B = p.n_buckets();
     const __nv_bfloat16* gsrc = grads ? (const __nv_bfloat16*)grads : h->grad;
     CUDA_TRY(h, cudaEventRecord(h->ev_start, s));
     CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_start, 0));
     mark(h, 1, s);
     sp.g32 = h->g32;
-    for (int64_t b = 0; b < B; ++b) {
+    for (int64_t b = b0; b < b1; ++b) {
         const int64_t base = p.buckets[4 * b], S = p.buckets[4 * b + 1];
         float* up = h->up32[b & 1];
-        // staging buffer b&1 is free once pass A of bucket b-2 ... the RS of bucket b-2 is done
-        // (the RS reads `up`), which comm_stream order already guarantees.
+        // the staging buffer is reused every other bucket; comm_stream order guarantees the
+        // reduce-scatter that read it has finished before the next upcast overwrites it
         LAUNCH(h, launch_upcast_bf16(gsrc + base, up, S, h->comm_stream));
         NCCL_TRY(h, ncclReduceScatter(up, h->g32 + p.shard_base[b], (size_t)(S / D), ncclFloat,
                                       ncclSum, h->comm, h->comm_stream));
@@ -551,7 +577,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     }
     if (pre) {
         // the global norm needs every bucket's reduced gradient: wait for all RS first
-        for (int64_t b = 0; b < B; ++b) CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_rs[b], 0));
+        for (int64_t b = b0; b < b1; ++b) CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_rs[b], 0));
         LAUNCH(h, launch_grad_stats(sp, 0, false, h->grid_a, s));
         LAUNCH(h, launch_clip_finalize(cp, s));
         double* rows = h->clip_rows(-1);
@@ -559,7 +585,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         LAUNCH(h, launch_clip_combine(cp, s));
         LAUNCH(h, launch_pass_a(sp, 0, true, h->grid_a, s));
     } else {
-        for (int64_t b = 0; b < B; ++b) {
+        for (int64_t b = b0; b < b1; ++b) {
             CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_rs[b], 0));
             sp.item_begin = h->bucket_item_begin[b];
             sp.item_end = h->bucket_item_begin[b + 1];
@@ -570,18 +596,19 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     for (int j = 0; j < D; ++j) fp.xrow[j] = h->xbuf(-1);
     LAUNCH(h, launch_finalize_segments(fp, s));
     mark(h, 3, s);
-    if (!p.straddlers.empty()) {
+    if (strad) {
         const size_t n = p.straddlers.size() * 2;
         double* xb = reinterpret_cast<double*>(h->xbuf(-1));
         NCCL_TRY(h, ncclAllGather(xb + (size_t)r * n, xb, n, ncclDouble, h->comm, s));
-        if (h->n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
+        if (fp.n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
     }
     mark(h, 4, s);
     sp.pdst[0] = h->param;
-    for (int64_t b = 0; b < B; ++b) {
+    for (int64_t b = b0; b < b1; ++b) {
         sp.item_begin = h->bucket_item_begin[b];
         sp.item_end = h->bucket_item_begin[b + 1];
         LAUNCH(h, launch_pass_b(sp, 1, h->grid_b, s));
+        if (defer_ag) continue;
         CUDA_TRY(h, cudaEventRecord(h->ev_b[b], s));
         CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_b[b], 0));
         const int64_t base = p.buckets[4 * b], sl = p.buckets[4 * b + 1] / D;
@@ -618,9 +645,48 @@ extern "C" lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void
     lamb_status st = check_async(h);
     if (st != LAMB_OK) return st;
     cudaSetDevice(h->device);
-    st = step_impl(h, grads, step, static_cast<cudaStream_t>(stream));
+    st = step_impl(h, grads, step, static_cast<cudaStream_t>(stream), 0, h->plan.n_buckets(), false);
     if (h->t_n < h->t_max) ++h->t_n;
     return st;
+}
+
+extern "C" lamb_status lamb_step_bucket(lamb_t h, int64_t bucket, int64_t step, int32_t flags, void* stream) {
+    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
+    if (bucket < 0 || bucket >= h->plan.n_buckets()) return fail(h, LAMB_EINVAL, "bucket out of range");
+    if (step < 1) return fail(h, LAMB_EINVAL, "step must be >= 1");
+    if (flags & ~LAMB_BUCKET_DEFER_AG) return fail(h, LAMB_EINVAL, "unknown flags");
+    if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step_bucket before lamb_set_master / lamb_synth_init");
+    lamb_status st = check_async(h);
+    if (st != LAMB_OK) return st;
+    cudaSetDevice(h->device);
+    const int32_t t_max = h->t_max;
+    h->t_max = 0;   // per-bucket calls are not phase-timed
+    st = step_impl(h, nullptr, step, static_cast<cudaStream_t>(stream), bucket, bucket + 1,
+                   (flags & LAMB_BUCKET_DEFER_AG) != 0);
+    h->t_max = t_max;
+    return st;
+}
+
+extern "C" lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream) {
+    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
+    if (bucket < 0 || bucket >= h->plan.n_buckets()) return fail(h, LAMB_EINVAL, "bucket out of range");
+    const Plan& p = h->plan;
+    const int D = p.world, r = p.rank;
+    if (D == 1) return LAMB_OK;
+    cudaSetDevice(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t base = p.buckets[4 * bucket], sl = p.buckets[4 * bucket + 1] / D;
+    if (h->cfg.comm_mode == LAMB_COMM_FUSED) {
+        // pull the peers' slices over NVLink; they were completed before the barrier that
+        // ended their lamb_step_bucket, and are not rewritten before this rank's next
+        // barrier of this bucket
+        LAUNCH(h, lamb::launch_gather(const_cast<const __nv_bfloat16* const*>(h->peer_param), h->param,
+                                      base, sl, D, r, s));
+        return LAMB_OK;
+    }
+    NCCL_TRY(h, ncclAllGather(h->param + base + (int64_t)r * sl, h->param + base, (size_t)sl,
+                              ncclBfloat16, h->comm, s));
+    return LAMB_OK;
 }
 
 extern "C" lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_params,

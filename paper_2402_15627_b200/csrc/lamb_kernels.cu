@@ -14,6 +14,7 @@
 // All three are HBM/NVLink streaming kernels (~1 flop/B): no tensor cores.  Design for B200:
 // 128-bit coalesced loads with L1::no_allocate, several independent chunks per lane in
 // flight, a persistent grid of (148 x resident CTAs) warps walking the item table.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -290,14 +291,34 @@ __device__ __forceinline__ void clip_state(double total, const ClipParams& P) {
     *P.out = cs;
 }
 
-// One CTA: fixed-order sum of all item partials of this rank; D = 1 -> clip state, else the
-// rank's row is stored into every rank's row buffer (slot `rank`).
-constexpr int kClipThreads = 1024;
+// Two-level fixed-order sum of all item partials of this rank: kClipBlocks CTAs each sum a
+// contiguous range of items (thread-strided, then a fixed tree) into block partials; the last
+// level runs in clip_finalize_kernel.  D = 1 -> clip state; else the rank's row is stored into
+// every rank's row buffer (slot `rank`).
+constexpr int kClipThreads = 256;
+constexpr int kClipBlocks = kClipBlocksMax;
+__global__ void __launch_bounds__(kClipThreads) clip_partial_kernel(const __grid_constant__ ClipParams P) {
+    __shared__ double red[kClipThreads];
+    const int tid = threadIdx.x;
+    const int64_t per = (P.n_items + kClipBlocks - 1) / kClipBlocks;
+    const int64_t lo = (int64_t)blockIdx.x * per;
+    const int64_t hi = lo + per < P.n_items ? lo + per : P.n_items;
+    double s = 0.0;
+    for (int64_t i = lo + tid; i < hi; i += kClipThreads) s += P.partials[i].x;
+    red[tid] = s;
+    __syncthreads();
+    for (int o = kClipThreads / 2; o > 0; o >>= 1) {
+        if (tid < o) red[tid] += red[tid + o];
+        __syncthreads();
+    }
+    if (tid == 0) P.block_sums[blockIdx.x] = red[0];
+}
+
 __global__ void __launch_bounds__(kClipThreads) clip_finalize_kernel(const __grid_constant__ ClipParams P) {
     __shared__ double red[kClipThreads];
     const int tid = threadIdx.x;
     double s = 0.0;
-    for (int64_t i = tid; i < P.n_items; i += kClipThreads) s += P.partials[i].x;
+    for (int i = tid; i < kClipBlocks; i += kClipThreads) s += P.block_sums[i];
     red[tid] = s;
     __syncthreads();
     for (int o = kClipThreads / 2; o > 0; o >>= 1) {
@@ -437,6 +458,25 @@ __global__ void barrier_kernel_v(const __grid_constant__ BarrierArgs A, uint64_t
             }
             __nanosleep(64);
         }
+    }
+}
+
+// ------------------------------------------------------------ deferred all-gather
+// Pull the D-1 peers' bf16 slices of one bucket over NVLink into the local param buffer
+// (16 B per lane; slices are multiples of 128 elements).
+struct GatherArgs {
+    const __nv_bfloat16* src[LAMB_MAX_RANKS];
+};
+__global__ void gather_kernel(const __grid_constant__ GatherArgs A, __nv_bfloat16* __restrict__ dst,
+                              int64_t base, int64_t slice, int world, int rank) {
+    const int64_t vec_per = slice / 8;
+    const int64_t total = vec_per * (world - 1);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int j = (int)(i / vec_per);
+        j += j >= rank;
+        const int64_t off = base + (int64_t)j * slice + (i % vec_per) * 8;
+        __stcs(reinterpret_cast<uint4*>(dst + off), __ldcs(reinterpret_cast<const uint4*>(A.src[j] + off)));
     }
 }
 
@@ -587,6 +627,9 @@ cudaError_t launch_grad_stats(const StepParams& p, int nsrc, bool mat, int grid,
 }
 
 cudaError_t launch_clip_finalize(const ClipParams& p, cudaStream_t s) {
+    clip_partial_kernel<<<kClipBlocks, kClipThreads, 0, s>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     clip_finalize_kernel<<<1, kClipThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
@@ -613,6 +656,17 @@ cudaError_t launch_barrier(uint64_t* const* flags, uint64_t* epoch, int rank, in
     BarrierArgs a;
     for (int j = 0; j < LAMB_MAX_RANKS; ++j) a.flags[j] = j < world ? flags[j] : nullptr;
     barrier_kernel_v<<<1, 32, 0, s>>>(a, epoch, rank, world, err_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const __nv_bfloat16* const* peers, __nv_bfloat16* dst, int64_t base, int64_t slice,
+                          int world, int rank, cudaStream_t s) {
+    GatherArgs a;
+    for (int j = 0; j < LAMB_MAX_RANKS; ++j) a.src[j] = j < world ? peers[j] : nullptr;
+    const int64_t total = slice / 8 * (world - 1);
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 8);
+    if (total <= 0) return cudaSuccess;
+    gather_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, dst, base, slice, world, rank);
     return cudaGetLastError();
 }
 

@@ -61,7 +61,9 @@ struct ClipParams {
     int32_t world, rank;
     float grad_scale, inv_loss_scale, max_grad_norm;
     ClipState* out;
+    double* block_sums;             // [kClipBlocks] scratch of the two-level sum
 };
+constexpr int kClipBlocksMax = 296;
 
 struct StepParams {
     const Item* items;
@@ -115,6 +117,8 @@ cudaError_t launch_finalize_segments(const FinalizeParams& p, cudaStream_t s);
 cudaError_t launch_finalize_straddlers(const FinalizeParams& p, cudaStream_t s);
 cudaError_t launch_barrier(uint64_t* const* flags, uint64_t* epoch, int rank, int world,
                            int* err_flag, cudaStream_t s);
+cudaError_t launch_gather(const __nv_bfloat16* const* peers, __nv_bfloat16* dst, int64_t base, int64_t slice,
+                          int world, int rank, cudaStream_t s);
 cudaError_t launch_upcast_bf16(const __nv_bfloat16* src, float* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_cast_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t s);
 int pass_grid(int device, int nsrc, bool g32, bool pass_b, int ndst);

@@ -29,6 +29,7 @@ LAMB_MAX_RANKS = 8
 LAMB_UNIQUE_ID_BYTES = 128
 LAMB_COMM_NCCL, LAMB_COMM_FUSED = 0, 1
 LAMB_FLAG_TIMING = 1
+LAMB_BUCKET_DEFER_AG = 1
 LAMB_BUF_GRAD, LAMB_BUF_PARAM, LAMB_BUF_W, LAMB_BUF_M, LAMB_BUF_V = range(5)
 PHASES = ["barrier_in", "pass_a", "finalize", "exchange", "pass_b", "barrier_out"]
 LAMB_N_PHASES = len(PHASES)
@@ -84,6 +85,8 @@ _SIGS = {
                           ctypes.c_int32, ctypes.POINTER(lamb_config), ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "lamb_step": (_st, [_vp, _vp, ctypes.c_int64, _vp]),
     "lamb_step_host": (_st, [_vp, _vp, _vp, ctypes.c_int64, _vp]),
+    "lamb_step_bucket": (_st, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _vp]),
+    "lamb_gather_bucket": (_st, [_vp, ctypes.c_int64, _vp]),
     "lamb_destroy": (None, [_vp]),
     "lamb_query_plan": (_st, [_vp, ctypes.POINTER(lamb_plan_view)]),
     "lamb_buffer": (_st, [_vp, ctypes.c_int32, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64)]),
@@ -256,6 +259,13 @@ class Lamb:
 
     def step(self, t: int, stream=None, grads_ptr: Optional[int] = None) -> None:
         check(lamb_step(self.h, grads_ptr, int(t), self._stream(stream)), self.h)
+
+    def step_bucket(self, bucket: int, t: int, defer_ag: bool = False, stream=None) -> None:
+        check(lamb_step_bucket(self.h, int(bucket), int(t), LAMB_BUCKET_DEFER_AG if defer_ag else 0,
+                               self._stream(stream)), self.h)
+
+    def gather_bucket(self, bucket: int, stream=None) -> None:
+        check(lamb_gather_bucket(self.h, int(bucket), self._stream(stream)), self.h)
 
     def step_host(self, host_grads, host_params, t: int, stream=None) -> None:
         check(lamb_step_host(self.h, ctypes.c_void_p(host_grads.data_ptr()),

@@ -110,6 +110,39 @@ def clip_case(world, rank, local, mode):
         print(f"[ok] clip D={world} mode={mode} (global norm, clip, skip on NaN)", flush=True)
 
 
+def bucket_case(world, rank, local, mode):
+    """Per-bucket stepping in backward order with the deferred all-gather == lamb_step, bitwise
+    on every rank (NEXT #2)."""
+    from paper_2402_15627_b200 import lamb
+    rng = np.random.default_rng(101)
+    tensors = W.random_table(rng, 50, max_numel=6000, p_big=0.2, big=40_000)
+    wl = W.Workload("bkd", 73, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    mk = lambda: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
+                           device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD)
+    A, B = mk(), mk()
+    nb = len(A.plan.buckets)
+    for L in (A, B):
+        L.synth_init(spec, wl.seed)
+    for t in (1, 2):
+        for L in (A, B):
+            L.synth_grads(spec, wl.seed, rank + 1, t)
+        A.step(t)
+        for b in reversed(range(nb)):
+            B.step_bucket(b, t, defer_ag=True)
+        for b in range(nb):
+            B.gather_bucket(b)
+    torch.cuda.synchronize()
+    for k in (2, 3, 4):
+        assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32)), k
+    assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
+    A.close()
+    B.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] per-bucket stepping D={world} mode={mode} buckets={nb} == lamb_step (bitwise)", flush=True)
+
+
 def ckpt_case(world, rank, local, mode):
     """Checkpoint saved by D ranks; reloaded (a) by D ranks with another bucket cap and
     (b) by rank 0 alone at D = 1 (reshard); both continue and must match the oracle."""
@@ -180,6 +213,7 @@ def main():
              cap=100_000)
     ckpt_case(world, rank, local, mode)
     clip_case(world, rank, local, mode)
+    bucket_case(world, rank, local, mode)
     if a.big:
         wl = W.gpt_1p3b()
         ids = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 289, 290]

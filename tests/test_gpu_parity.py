@@ -331,3 +331,38 @@ def test_prestep_nonfinite_skip(lamb):
     L.step(2)
     assert not L.step_info()["skipped"]
     L.close()
+
+
+@pytest.mark.parametrize("defer", [False, True])
+def test_step_bucket_equals_step(lamb, defer):
+    """NEXT #2: stepping every bucket in backward (reverse) order is bit-identical to one
+    lamb_step (per-bucket LAMB is exact: a tensor never spans buckets)."""
+    rng = np.random.default_rng(55)
+    tensors = W.random_table(rng, 40, max_numel=6000, p_big=0.2, big=40_000)
+    wl = W.Workload("bk", 95, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    A = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=15_000)
+    B = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=15_000)
+    nb = len(A.plan.buckets)
+    assert nb > 3
+    for L in (A, B):
+        L.synth_init(spec, wl.seed)
+    for t in (1, 2, 3):
+        for L in (A, B):
+            L.synth_grads(spec, wl.seed, 1, t)
+        A.step(t)
+        for b in reversed(range(nb)):
+            B.step_bucket(b, t, defer_ag=defer)
+        if defer:
+            for b in range(nb):
+                B.gather_bucket(b)
+    torch.cuda.synchronize()
+    for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V):
+        assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32))
+    assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
+    B.set_grad_clip(1.0)
+    with pytest.raises(lamb.LambError) as e:
+        B.step_bucket(0, 4)
+    assert e.value.status == lamb.LAMB_EUNSUPPORTED
+    A.close()
+    B.close()

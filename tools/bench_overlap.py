@@ -1,0 +1,140 @@
+"""NEXT #2 measurement: overlap of the sharded LAMB step with a synthetic forward/backward, the
+paper's DP overlap (§3.2: RS of a chunk right after its backward, AG right
+before its forward, the first AG prefetched, priority = order of the dependent compute).
+
+The forward/backward is a synthetic compute load: per bucket b, bf16 GEMMs (cuBLAS via torch,
+a plain library GEMM standing in for the model) worth 2*P_b*tokens FLOPs forward and twice that
+backward.  Three iteration schedules, timed with CUDA events on the compute stream, max over
+ranks:
+  compute  - forward + backward only (the floor),
+  serial   - forward + backward, then lamb_step (RS + update + AG exposed),
+  overlap  - per bucket: lamb_step_bucket(b, defer AG) on a second stream as soon as b's
+             backward is done; lamb_gather_bucket(b) before b's next forward (prefetched in
+             bucket order at the start of the iteration).
+    python tools/bench_overlap.py --config gpt1.3b --tokens 4096
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/bench_overlap.py
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import workloads as W  # noqa: E402
+from paper_2402_15627_b200 import lamb  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="gpt1.3b")
+ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU per iteration")
+ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--warmup", type=int, default=2)
+a = ap.parse_args()
+
+world = int(os.environ.get("WORLD_SIZE", "1"))
+rank = int(os.environ.get("RANK", "0"))
+local = int(os.environ.get("LOCAL_RANK", "0"))
+torch.cuda.set_device(local)
+pg = None
+if world > 1:
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pg = dist.group.WORLD
+
+wl = W.get(a.config)
+spec = [(t.init, t.gexp) for t in wl.tensors]
+L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
+              device=local, bucket_cap=wl.cap, pg=pg)
+L.synth_init(spec, wl.seed)
+L.synth_grads(spec, wl.seed, rank + 1, 1)
+B = len(L.plan.buckets)
+params_b = [sum(wl.tensors[i].numel for i in range(int(t0), int(t1))) for (_, _, t0, t1) in L.plan.buckets.tolist()]
+
+# synthetic compute: GEMM [tokens, K] x [K, K]
+K = 2048
+X = torch.randn(a.tokens, K, device="cuda", dtype=torch.bfloat16)
+Wm = torch.randn(K, K, device="cuda", dtype=torch.bfloat16)
+Y = torch.empty(a.tokens, K, device="cuda", dtype=torch.bfloat16)
+gemm_flops = 2.0 * a.tokens * K * K
+reps_f = [max(1, round(2.0 * P * a.tokens / gemm_flops)) for P in params_b]
+
+
+def gemms(n):
+    for _ in range(n):
+        torch.matmul(X, Wm, out=Y)
+
+
+comp = torch.cuda.current_stream()
+ls = torch.cuda.Stream()
+ev_grad = [torch.cuda.Event() for _ in range(B)]
+ev_gath = [torch.cuda.Event() for _ in range(B)]
+ev_ls_done = torch.cuda.Event()
+step = [0]
+
+
+def iteration(mode):
+    step[0] += 1
+    t = step[0]
+    if mode == "overlap":
+        # forward: gathers issued in bucket order (the first is the prefetch), each forward waits
+        with torch.cuda.stream(ls):
+            for b in range(B):
+                L.gather_bucket(b, stream=ls)
+                ev_gath[b].record(ls)
+        for b in range(B):
+            comp.wait_event(ev_gath[b])
+            gemms(reps_f[b])
+        for b in reversed(range(B)):
+            gemms(2 * reps_f[b])
+            ev_grad[b].record(comp)
+            ls.wait_event(ev_grad[b])
+            L.step_bucket(b, t, defer_ag=True, stream=ls)
+        ev_ls_done.record(ls)
+        comp.wait_event(ev_ls_done)
+    else:
+        for b in range(B):
+            gemms(reps_f[b])
+        for b in reversed(range(B)):
+            gemms(2 * reps_f[b])
+        if mode == "serial":
+            L.step(t, stream=comp)
+
+
+def timed(mode):
+    for _ in range(a.warmup):
+        iteration(mode)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    for _ in range(a.iters):
+        iteration(mode)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.iters
+    if world > 1:
+        x = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        ms = float(x)
+    return ms
+
+
+res = {}
+for m in ("compute", "serial", "overlap"):
+    res[m] = timed(m)
+res["compute"] = min(res["compute"], timed("compute"))
+if rank == 0:
+    exposed_serial = res["serial"] - res["compute"]
+    exposed_overlap = res["overlap"] - res["compute"]
+    print(json.dumps({"config": wl.name, "n_gpus": world, "tokens_per_gpu": a.tokens, "buckets": B,
+                      "compute_tflop_per_iter": 3 * sum(reps_f) * gemm_flops / 1e12,
+                      "ms_compute": res["compute"], "ms_serial": res["serial"], "ms_overlap": res["overlap"],
+                      "exposed_ms_serial": exposed_serial, "exposed_ms_overlap": exposed_overlap,
+                      "hidden_frac": 1.0 - exposed_overlap / exposed_serial if exposed_serial > 0 else None}))
+L.close()
+if world > 1:
+    dist.barrier()
+    dist.destroy_process_group()
