@@ -154,6 +154,10 @@ lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_
  * EINVAL: bucket out of range, step < 1, unknown flags.  ESTATE: master not set.
  * EUNSUPPORTED: the pre-step is enabled (its global norm needs the whole table). */
 lamb_status lamb_step_bucket(lamb_t h, int64_t bucket, int64_t step, int32_t flags, void* stream);
+/* SM budget: caps the persistent grid of the streaming passes at max_ctas CTAs (256 threads;
+ * 0 = one full wave, the default) so that a concurrently running compute stream keeps the
+ * remaining SMs.  Applies to subsequent lamb_step / lamb_step_bucket calls.  EINVAL: < 0. */
+lamb_status lamb_set_max_ctas(lamb_t h, int32_t max_ctas);
 /* Deferred all-gather of one bucket's bf16 params (FUSED: NVLink pull of the D-1 peer slices;
  * NCCL: ncclAllGather, COLLECTIVE).  No-op at D = 1. */
 lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream);

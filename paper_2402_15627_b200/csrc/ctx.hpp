@@ -70,6 +70,7 @@ struct lamb_ctx {
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t ev_h2d = nullptr, ev_params = nullptr, ev_d2h = nullptr;
     int grid_a = 0, grid_b = 0;
+    int max_ctas = 0;   // SM budget of the streaming passes (0 = one full wave)
     // synth tables (device)
     int64_t *d_tensor_off = nullptr, *d_numel = nullptr, *d_shard_base = nullptr,
             *d_bucket_base = nullptr, *d_bucket_slice = nullptr;

@@ -450,6 +450,9 @@ static inline void mark(lamb_ctx* h, int phase, cudaStream_t s) {
 static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStream_t s, int64_t b0,
                              int64_t b1, bool defer_ag) {
     const Plan& p = h->plan;
+    // SM budget (lamb_set_max_ctas): fewer persistent CTAs leave SMs to concurrent compute
+    const int grid_a = h->max_ctas > 0 ? std::min(h->max_ctas, h->grid_a) : h->grid_a;
+    const int grid_b = h->max_ctas > 0 ? std::min(h->max_ctas, h->grid_b) : h->grid_b;
     const int D = h->cfg.world_size, r = h->cfg.rank;
     const bool fused = D > 1 && h->cfg.comm_mode == LAMB_COMM_FUSED;
     const bool nccl = D > 1 && h->cfg.comm_mode == LAMB_COMM_NCCL;
@@ -522,18 +525,18 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         if (pre) {
             // pre-step: global ||g||^2 (FUSED: the reduce-scatter happens here, into g32)
             sp.g32_out = h->g32;
-            LAUNCH(h, launch_grad_stats(sp, D, fused, h->grid_a, s));
+            LAUNCH(h, launch_grad_stats(sp, D, fused, grid_a, s));
             LAUNCH(h, launch_clip_finalize(cp, s));
             if (fused) {
                 LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
                 LAUNCH(h, launch_clip_combine(cp, s));
                 sp.g32 = h->g32;
-                LAUNCH(h, launch_pass_a(sp, 0, true, h->grid_a, s));
+                LAUNCH(h, launch_pass_a(sp, 0, true, grid_a, s));
             } else {
-                LAUNCH(h, launch_pass_a(sp, D, false, h->grid_a, s));
+                LAUNCH(h, launch_pass_a(sp, D, false, grid_a, s));
             }
         } else {
-            LAUNCH(h, launch_pass_a(sp, D, false, h->grid_a, s));
+            LAUNCH(h, launch_pass_a(sp, D, false, grid_a, s));
         }
         if (!fused) CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));   // D = 1: grads consumed
         mark(h, 2, s);
@@ -548,7 +551,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         mark(h, 4, s);
         const bool push = fused && !defer_ag;
         for (int j = 0; j < D; ++j) sp.pdst[j] = push ? h->peer_param[j] : h->param;
-        LAUNCH(h, launch_pass_b(sp, push ? D : 1, h->grid_b, s));
+        LAUNCH(h, launch_pass_b(sp, push ? D : 1, grid_b, s));
         mark(h, 5, s);
         if (fused) {
             // params complete everywhere, and every rank finished reading this rank's grads
@@ -578,18 +581,18 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     if (pre) {
         // the global norm needs every bucket's reduced gradient: wait for all RS first
         for (int64_t b = b0; b < b1; ++b) CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_rs[b], 0));
-        LAUNCH(h, launch_grad_stats(sp, 0, false, h->grid_a, s));
+        LAUNCH(h, launch_grad_stats(sp, 0, false, grid_a, s));
         LAUNCH(h, launch_clip_finalize(cp, s));
         double* rows = h->clip_rows(-1);
         NCCL_TRY(h, ncclAllGather(rows + r, rows, 1, ncclDouble, h->comm, s));
         LAUNCH(h, launch_clip_combine(cp, s));
-        LAUNCH(h, launch_pass_a(sp, 0, true, h->grid_a, s));
+        LAUNCH(h, launch_pass_a(sp, 0, true, grid_a, s));
     } else {
         for (int64_t b = b0; b < b1; ++b) {
             CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_rs[b], 0));
             sp.item_begin = h->bucket_item_begin[b];
             sp.item_end = h->bucket_item_begin[b + 1];
-            LAUNCH(h, launch_pass_a(sp, 0, true, h->grid_a, s));
+            LAUNCH(h, launch_pass_a(sp, 0, true, grid_a, s));
         }
     }
     mark(h, 2, s);
@@ -607,7 +610,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     for (int64_t b = b0; b < b1; ++b) {
         sp.item_begin = h->bucket_item_begin[b];
         sp.item_end = h->bucket_item_begin[b + 1];
-        LAUNCH(h, launch_pass_b(sp, 1, h->grid_b, s));
+        LAUNCH(h, launch_pass_b(sp, 1, grid_b, s));
         if (defer_ag) continue;
         CUDA_TRY(h, cudaEventRecord(h->ev_b[b], s));
         CUDA_TRY(h, cudaStreamWaitEvent(h->comm_stream, h->ev_b[b], 0));
@@ -797,6 +800,13 @@ extern "C" lamb_status lamb_set_lr(lamb_t h, int32_t group, float lr) {
     if (group < 0 || group >= (int32_t)h->groups.size()) return fail(h, LAMB_EINVAL, "group out of range");
     if (!(lr >= 0.f)) return fail(h, LAMB_EINVAL, "lr must be >= 0");
     h->groups[group].lr = lr;
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_set_max_ctas(lamb_t h, int32_t max_ctas) {
+    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
+    if (max_ctas < 0) return fail(h, LAMB_EINVAL, "max_ctas must be >= 0");
+    h->max_ctas = max_ctas;
     return LAMB_OK;
 }
 

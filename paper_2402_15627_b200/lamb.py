@@ -87,6 +87,7 @@ _SIGS = {
     "lamb_step_host": (_st, [_vp, _vp, _vp, ctypes.c_int64, _vp]),
     "lamb_step_bucket": (_st, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _vp]),
     "lamb_gather_bucket": (_st, [_vp, ctypes.c_int64, _vp]),
+    "lamb_set_max_ctas": (_st, [_vp, ctypes.c_int32]),
     "lamb_destroy": (None, [_vp]),
     "lamb_query_plan": (_st, [_vp, ctypes.POINTER(lamb_plan_view)]),
     "lamb_buffer": (_st, [_vp, ctypes.c_int32, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64)]),
@@ -263,6 +264,9 @@ class Lamb:
     def step_bucket(self, bucket: int, t: int, defer_ag: bool = False, stream=None) -> None:
         check(lamb_step_bucket(self.h, int(bucket), int(t), LAMB_BUCKET_DEFER_AG if defer_ag else 0,
                                self._stream(stream)), self.h)
+
+    def set_max_ctas(self, max_ctas: int) -> None:
+        check(lamb_set_max_ctas(self.h, int(max_ctas)), self.h)
 
     def gather_bucket(self, bucket: int, stream=None) -> None:
         check(lamb_gather_bucket(self.h, int(bucket), self._stream(stream)), self.h)

@@ -32,6 +32,7 @@ ap.add_argument("--config", default="gpt1.3b")
 ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU per iteration")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=2)
+ap.add_argument("--ctas", default="0,148,74,37", help="SM budgets (max CTAs) to try in overlap mode")
 a = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -67,7 +68,7 @@ def gemms(n):
 
 
 comp = torch.cuda.current_stream()
-ls = torch.cuda.Stream()
+ls = torch.cuda.Stream(priority=-1)   # the paper's "high priority communication first"
 ev_grad = [torch.cuda.Event() for _ in range(B)]
 ev_gath = [torch.cuda.Event() for _ in range(B)]
 ev_ls_done = torch.cuda.Event()
@@ -123,15 +124,22 @@ def timed(mode):
 
 
 res = {}
-for m in ("compute", "serial", "overlap"):
+for m in ("compute", "serial"):
     res[m] = timed(m)
+over = {}
+for c in [int(x) for x in a.ctas.split(",")]:
+    L.set_max_ctas(c)
+    over[c] = timed("overlap")
+L.set_max_ctas(0)
 res["compute"] = min(res["compute"], timed("compute"))
 if rank == 0:
     exposed_serial = res["serial"] - res["compute"]
-    exposed_overlap = res["overlap"] - res["compute"]
+    best = min(over, key=over.get)
+    exposed_overlap = over[best] - res["compute"]
     print(json.dumps({"config": wl.name, "n_gpus": world, "tokens_per_gpu": a.tokens, "buckets": B,
                       "compute_tflop_per_iter": 3 * sum(reps_f) * gemm_flops / 1e12,
-                      "ms_compute": res["compute"], "ms_serial": res["serial"], "ms_overlap": res["overlap"],
+                      "ms_compute": res["compute"], "ms_serial": res["serial"],
+                      "ms_overlap_by_max_ctas": over, "best_max_ctas": best, "ms_overlap": over[best],
                       "exposed_ms_serial": exposed_serial, "exposed_ms_overlap": exposed_overlap,
                       "hidden_frac": 1.0 - exposed_overlap / exposed_serial if exposed_serial > 0 else None}))
 L.close()

@@ -1,0 +1,116 @@
+// p2p_bench.cu — single-process NVLink microbenchmark for the fused passes' access patterns.
+// Every GPU g pulls (loads) or pushes (stores) `bytes` from/to each of the other D-1 GPUs at
+// the same time (the all-to-all shape of pass A's reduce-scatter / pass B's all-gather),
+// with 8 B or 16 B per lane.  Reports the per-GPU in-bound GB/s.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/p2p_bench tools/p2p_bench.cu
+//   tools/p2p_bench <D> <MiB per peer>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                       \
+    do {                                                                            \
+        cudaError_t e = (x);                                                        \
+        if (e != cudaSuccess) {                                                     \
+            fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); \
+            exit(1);                                                                \
+        }                                                                           \
+    } while (0)
+
+struct Ptrs {
+    const char* src[8];
+    char* dst[8];
+};
+
+template <typename V, bool PUSH>
+__global__ void a2a(Ptrs P, int D, int me, size_t bytes_per_peer, char* local) {
+    const size_t nv = bytes_per_peer / sizeof(V);
+    const size_t total = nv * (D - 1);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int j = (int)(i / nv);
+        j += j >= me;
+        const size_t k = i % nv;
+        if (PUSH) {
+            // store my data into peer j's buffer (slot me)
+            reinterpret_cast<V*>(P.dst[j] + (size_t)me * bytes_per_peer)[k] =
+                reinterpret_cast<const V*>(local + (size_t)j * bytes_per_peer)[k];
+        } else {
+            reinterpret_cast<V*>(local + (size_t)j * bytes_per_peer)[k] =
+                __ldcs(reinterpret_cast<const V*>(P.src[j] + (size_t)me * bytes_per_peer) + k);
+        }
+    }
+}
+
+template <typename V, bool PUSH>
+float run(int D, size_t bpp, std::vector<char*>& remote, std::vector<char*>& local, int grid) {
+    std::vector<cudaEvent_t> e0(D), e1(D);
+    for (int g = 0; g < D; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaEventCreate(&e0[g]));
+        CK(cudaEventCreate(&e1[g]));
+    }
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaDeviceSynchronize());
+        }
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            Ptrs P;
+            for (int j = 0; j < D; ++j) {
+                P.src[j] = remote[j];
+                P.dst[j] = remote[j];
+            }
+            CK(cudaEventRecord(e0[g]));
+            a2a<V, PUSH><<<grid, 256>>>(P, D, g, bpp, local[g]);
+            CK(cudaEventRecord(e1[g]));
+        }
+        float worst = 0;
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaEventSynchronize(e1[g]));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0[g], e1[g]));
+            worst = ms > worst ? ms : worst;
+        }
+        best = worst < best ? worst : best;
+    }
+    return (float)(bpp * (D - 1)) / (best * 1e-3f) / 1e9f;
+}
+
+int main(int argc, char** argv) {
+    const int D = argc > 1 ? atoi(argv[1]) : 2;
+    const size_t mib = argc > 2 ? (size_t)atoll(argv[2]) : 512;
+    const size_t bpp = mib << 20;
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (n < D) {
+        fprintf(stderr, "need %d GPUs, have %d\n", D, n);
+        return 1;
+    }
+    std::vector<char*> remote(D), local(D);
+    int sms = 0;
+    for (int g = 0; g < D; ++g) {
+        CK(cudaSetDevice(g));
+        for (int j = 0; j < D; ++j)
+            if (j != g) CK(cudaDeviceEnablePeerAccess(j, 0));
+        CK(cudaMalloc(&remote[g], bpp * D));
+        CK(cudaMalloc(&local[g], bpp * D));
+        CK(cudaMemset(remote[g], 1, bpp * D));
+        CK(cudaMemset(local[g], 2, bpp * D));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g));
+    }
+    printf("{\"D\": %d, \"MiB_per_peer\": %zu", D, mib);
+    for (int mult : {4, 8, 16}) {
+        const int grid = sms * mult;
+        printf(", \"pull8_x%d\": %.1f", mult, run<uint2, false>(D, bpp, remote, local, grid));
+        printf(", \"pull16_x%d\": %.1f", mult, run<uint4, false>(D, bpp, remote, local, grid));
+        printf(", \"push8_x%d\": %.1f", mult, run<uint2, true>(D, bpp, remote, local, grid));
+        printf(", \"push16_x%d\": %.1f", mult, run<uint4, true>(D, bpp, remote, local, grid));
+    }
+    printf("}\n");
+    return 0;
+}
