@@ -32,7 +32,9 @@ ap.add_argument("--config", default="gpt1.3b")
 ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU per iteration")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=2)
-ap.add_argument("--ctas", default="0,148,74,37", help="SM budgets (max CTAs) to try in overlap mode")
+ap.add_argument("--ctas", default="0,74,37", help="SM budgets (max CTAs) to try in overlap mode")
+ap.add_argument("--cap", type=int, default=0, help="bucket cap (0 = the workload's)")
+ap.add_argument("--K", type=int, default=2048, help="synthetic GEMM size [tokens,K]x[K,K]")
 a = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -47,14 +49,14 @@ if world > 1:
 wl = W.get(a.config)
 spec = [(t.init, t.gexp) for t in wl.tensors]
 L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
-              device=local, bucket_cap=wl.cap, pg=pg)
+              device=local, bucket_cap=a.cap or wl.cap, pg=pg)
 L.synth_init(spec, wl.seed)
 L.synth_grads(spec, wl.seed, rank + 1, 1)
 B = len(L.plan.buckets)
 params_b = [sum(wl.tensors[i].numel for i in range(int(t0), int(t1))) for (_, _, t0, t1) in L.plan.buckets.tolist()]
 
 # synthetic compute: GEMM [tokens, K] x [K, K]
-K = 2048
+K = a.K
 X = torch.randn(a.tokens, K, device="cuda", dtype=torch.bfloat16)
 Wm = torch.randn(K, K, device="cuda", dtype=torch.bfloat16)
 Y = torch.empty(a.tokens, K, device="cuda", dtype=torch.bfloat16)
@@ -101,6 +103,9 @@ def iteration(mode):
             gemms(2 * reps_f[b])
         if mode == "serial":
             L.step(t, stream=comp)
+        elif mode == "serial_buckets":   # per-bucket overhead without any overlap
+            for b in reversed(range(B)):
+                L.step_bucket(b, t, stream=comp)
 
 
 def timed(mode):
@@ -124,7 +129,7 @@ def timed(mode):
 
 
 res = {}
-for m in ("compute", "serial"):
+for m in ("compute", "serial", "serial_buckets"):
     res[m] = timed(m)
 over = {}
 for c in [int(x) for x in a.ctas.split(",")]:
@@ -139,6 +144,7 @@ if rank == 0:
     print(json.dumps({"config": wl.name, "n_gpus": world, "tokens_per_gpu": a.tokens, "buckets": B,
                       "compute_tflop_per_iter": 3 * sum(reps_f) * gemm_flops / 1e12,
                       "ms_compute": res["compute"], "ms_serial": res["serial"],
+                      "ms_serial_buckets": res["serial_buckets"], "K": K, "cap": a.cap or wl.cap,
                       "ms_overlap_by_max_ctas": over, "best_max_ctas": best, "ms_overlap": over[best],
                       "exposed_ms_serial": exposed_serial, "exposed_ms_overlap": exposed_overlap,
                       "hidden_frac": 1.0 - exposed_overlap / exposed_serial if exposed_serial > 0 else None}))

@@ -26,14 +26,14 @@ struct Ptrs {
 
 template <typename V, bool PUSH>
 __global__ void a2a(Ptrs P, int D, int me, size_t bytes_per_peer, char* local) {
+    // peers round-robin over the grid's blocks: block b serves peer (me + 1 + b % (D-1)) % D
     const size_t nv = bytes_per_peer / sizeof(V);
-    const size_t total = nv * (D - 1);
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        int j = (int)(i / nv);
-        j += j >= me;
-        const size_t k = i % nv;
+    const int np = D - 1;
+    const int j = (me + 1 + (int)(blockIdx.x % np)) % D;
+    const size_t nb = gridDim.x / np;
+    const size_t b = blockIdx.x / np;
+    for (size_t k = b * blockDim.x + threadIdx.x; k < nv; k += nb * blockDim.x) {
         if (PUSH) {
-            // store my data into peer j's buffer (slot me)
             reinterpret_cast<V*>(P.dst[j] + (size_t)me * bytes_per_peer)[k] =
                 reinterpret_cast<const V*>(local + (size_t)j * bytes_per_peer)[k];
         } else {
@@ -104,7 +104,7 @@ int main(int argc, char** argv) {
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g));
     }
     printf("{\"D\": %d, \"MiB_per_peer\": %zu", D, mib);
-    for (int mult : {4, 8, 16}) {
+    for (int mult : {3, 6, 12}) {   // multiples of 3 so every peer gets the same block count
         const int grid = sms * mult;
         printf(", \"pull8_x%d\": %.1f", mult, run<uint2, false>(D, bpp, remote, local, grid));
         printf(", \"pull16_x%d\": %.1f", mult, run<uint4, false>(D, bpp, remote, local, grid));
