@@ -62,10 +62,12 @@ def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, chec
         got = p.cpu().numpy().view(np.uint16)
         bad = np.nonzero(got != exp)[0]
         assert bad.size == 0, f"{name}: param mismatch at {bad[:5]} got {got[bad[:5]]} exp {exp[bad[:5]]}"
-    h = torch.tensor([int(p.long().sum().item()), int((p.long() * torch.arange(p.numel(), device=p.device) % 1000003).sum().item())],
-                     device="cuda")
-    hs = [torch.empty_like(h) for _ in range(world)]
-    dist.all_gather(hs, h)
+    # identical on every rank: sampled windows (same positions everywhere) compared across ranks
+    g = torch.Generator().manual_seed(7)
+    starts = torch.randint(0, max(1, p.numel() - 4096), (64,), generator=g).tolist()
+    win = torch.cat([p[s0:s0 + 4096] for s0 in starts] + [p[-4096:]]).long()
+    hs = [torch.empty_like(win) for _ in range(world)]
+    dist.all_gather(hs, win)
     assert all(torch.equal(x, hs[0]) for x in hs), f"{name}: param buffers differ across ranks"
     n_strad = len(L.plan.straddlers)
     L.close()
@@ -193,6 +195,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mode", default="fused", choices=["fused", "nccl"])
     ap.add_argument("--big", action="store_true", help="also run the 1.3B layout (sampled)")
+    ap.add_argument("--full", action="store_true",
+                    help="only the full-size BASELINE configs: 530B+stress (all stress tensors and "
+                         "LayerNorm tensors checked) and 13B (sampled), in the bench launch config")
     a = ap.parse_args()
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -202,6 +207,16 @@ def main():
     from paper_2402_15627_b200 import lamb
     mode = lamb.LAMB_COMM_FUSED if a.mode == "fused" else lamb.LAMB_COMM_NCCL
 
+    if a.full:
+        wl = W.slice_530b_stress()
+        ids = [i for i, t in enumerate(wl.tensors) if t.numel <= 20480]   # stress + LN/bias vectors
+        run_case("530b_stress(full size)", wl, world, rank, local, mode, 2, ids=ids, check_all_params=False)
+        wl = W.gpt_13b()
+        ids = [1, 2, 3, 4, 6, 7, 8, 10, 12, 13, 14, 481, 482]
+        run_case("gpt13b(full size)", wl, world, rank, local, mode, 1, ids=ids, check_all_params=False)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     run_case("toy", W.toy(), world, rank, local, mode, 1)
     run_case("toy10", W.toy(), world, rank, local, mode, 10)
     rng = np.random.default_rng(321)

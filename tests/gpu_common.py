@@ -46,11 +46,19 @@ def tol(steps):
 def compare_state(L, orc: oracle.OracleRun, steps: int, ids=None, check_params=True):
     """Compare this rank's pieces of w, m, v (and params/ratios) with the oracle."""
     rtol = tol(steps)
-    w = L.get_state(lamb_mod().LAMB_BUF_W)
-    m = L.get_state(lamb_mod().LAMB_BUF_M)
-    v = L.get_state(lamb_mod().LAMB_BUF_V)
-    ids = set(orc.ids) if ids is None else set(ids)
-    pw, pm, pv = shard_to_tensors(L, w, ids), shard_to_tensors(L, m, ids), shard_to_tensors(L, v, ids)
+    lm = lamb_mod()
+    if ids is None:
+        ids = set(orc.ids)
+        w, m, v = (L.get_state(k) for k in (lm.LAMB_BUF_W, lm.LAMB_BUF_M, lm.LAMB_BUF_V))
+        pw, pm, pv = shard_to_tensors(L, w, ids), shard_to_tensors(L, m, ids), shard_to_tensors(L, v, ids)
+    else:   # large configs: fetch only the checked segments from the device
+        ids = set(ids)
+        pw, pm, pv = {}, {}, {}
+        bufs = [L.state_buffer(k) for k in (lm.LAMB_BUF_W, lm.LAMB_BUF_M, lm.LAMB_BUF_V)]
+        for (i, soff, toff, ln) in L.plan.segments.tolist():
+            if i in ids:
+                for d, buf in zip((pw, pm, pv), bufs):
+                    d.setdefault(i, []).append((toff, buf[soff:soff + ln].cpu().numpy()))
     w2, u2, ratio = L.tensor_stats()
     params = L.param_buffer().view(__import__("torch").int16).cpu().numpy().view(np.uint16) if check_params else None
     worst = 0.0

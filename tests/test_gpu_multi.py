@@ -37,3 +37,10 @@ def test_parity_4gpu(mode):
 @pytest.mark.skipif(NGPU < 8, reason="needs 8 GPUs")
 def test_parity_8gpu_fused():
     _torchrun(8, "--mode", "fused", "--big")
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs >= 4 GPUs")
+def test_full_size_530b_stress_and_13b_4gpu():
+    """BASELINE configs[2] and [4] at full size on 4 GPUs (141 GB/GPU for 530B+stress): every
+    stress / LayerNorm tensor of the 530B slice and sampled 13B tensors against the oracle."""
+    _torchrun(4, "--mode", "fused", "--full", timeout=1800)

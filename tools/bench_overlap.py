@@ -33,6 +33,8 @@ ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU per ite
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--ctas", default="0,74,37", help="SM budgets (max CTAs) to try in overlap mode")
+ap.add_argument("--carveouts", default="8,16,32",
+                help="cuBLAS SM carve-outs to try (LAMB gets max_ctas = 2 x carve-out)")
 ap.add_argument("--cap", type=int, default=0, help="bucket cap (0 = the workload's)")
 ap.add_argument("--K", type=int, default=2048, help="synthetic GEMM size [tokens,K]x[K,K]")
 a = ap.parse_args()
@@ -135,6 +137,13 @@ over = {}
 for c in [int(x) for x in a.ctas.split(",")]:
     L.set_max_ctas(c)
     over[c] = timed("overlap")
+for k in [int(x) for x in a.carveouts.split(",") if x]:
+    # the GEMMs leave k SMs free (cuBLAS SM-count target); the LAMB passes take exactly those
+    torch._C._set_sm_carveout_experimental(k)
+    L.set_max_ctas(2 * k)
+    over[f"carveout{k}"] = timed("overlap")
+    res[f"compute_carveout{k}"] = timed("compute")
+    torch._C._set_sm_carveout_experimental(0)
 L.set_max_ctas(0)
 res["compute"] = min(res["compute"], timed("compute"))
 if rank == 0:
@@ -145,6 +154,7 @@ if rank == 0:
                       "compute_tflop_per_iter": 3 * sum(reps_f) * gemm_flops / 1e12,
                       "ms_compute": res["compute"], "ms_serial": res["serial"],
                       "ms_serial_buckets": res["serial_buckets"], "K": K, "cap": a.cap or wl.cap,
+                      "ms_compute_with_carveout": {k: v for k, v in res.items() if k.startswith("compute_carveout")},
                       "ms_overlap_by_max_ctas": over, "best_max_ctas": best, "ms_overlap": over[best],
                       "exposed_ms_serial": exposed_serial, "exposed_ms_overlap": exposed_overlap,
                       "hidden_frac": 1.0 - exposed_overlap / exposed_serial if exposed_serial > 0 else None}))
