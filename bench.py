@@ -27,7 +27,13 @@ import workloads as W  # noqa: E402
 METRIC = "LAMB params updated/sec & step ms at 1/2/4/8 B200; % HBM roofline"
 UNIT = "params/s"
 FALLBACK_HBM_GBS = 6650.0
-NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md measured peer copy per direction
+NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md measured peer copy per direction (context)
+# Per-GPU in-bound NVLink bandwidth of an all-to-all where every GPU pulls (loads) from / pushes
+# (stores) to every peer at once — the shape of the fused reduce-scatter (pass A) and
+# all-gather (pass B).  Measured on this pool with tools/p2p_bench.cu, 16 B per lane, D = 2 and
+# 4 (profiles/r01/p2p_all2all_D*.json): pull 624-633 GB/s, push 695-700 GB/s.
+NVLINK_PULL_GBS = 633.0
+NVLINK_PUSH_GBS = 700.0
 
 
 def parse():
@@ -258,22 +264,46 @@ def main():
     owned = int(sum(s[3] for s in L.plan.segments.tolist()))   # tensor elements this rank owns
     D = world
     fused = D > 1 and comm == lamb.LAMB_COMM_FUSED
-    bytes_a = owned * (20 + (2 if D == 1 or fused else 4))   # w r, m rw, v rw + own grad (bf16|fp32)
-    bytes_b = owned * (16 + 2)                               # m r, v r, w rw, p w (own slice)
+    n_flat = int(L.plan.flat_size)
+    # local HBM bytes per launch: own state (w r, m rw, v rw = 20 B) + gradients: D = 1 reads its
+    # bf16 grads (2 B); FUSED reads its whole flat grad buffer once across all D readers (2 B x
+    # flat / owned per element); NCCL mode reads the fp32 reduced shard (4 B)
+    grad_b = 2 * owned if D == 1 else (2 * n_flat if fused else 4 * owned)
+    bytes_a = 20 * owned + grad_b
+    bytes_b = 16 * owned + (2 * n_flat if fused else 2 * owned)   # m r, v r, w rw + params written
+    nvl_in = 2 * owned * (D - 1) if fused else 0                  # NVLink in per GPU per pass
     t_a, t_b = float(ph_mean[1]), float(ph_mean[4])
-    dom, t_dom, bytes_dom = ("pass_a", t_a, bytes_a) if t_a >= t_b else ("pass_b", t_b, bytes_b)
-    achieved = bytes_dom / (t_dom / 1e3) / 1e9
+
+    def pass_roof(name, nbytes, ms, nvl_peak):
+        hbm_gbps = nbytes / (ms / 1e3) / 1e9
+        out = {"kernel": name, "ms": ms, "bytes": nbytes, "GBps": hbm_gbps, "hbm_frac": hbm_gbps / hbm}
+        if nvl_in:
+            nvl_gbps = nvl_in / (ms / 1e3) / 1e9
+            out.update({"nvlink_in_bytes": nvl_in, "nvlink_GBps": nvl_gbps, "nvlink_peak": nvl_peak,
+                        "nvlink_frac": nvl_gbps / nvl_peak})
+        # the binding resource: the one whose bytes need the longer time at its peak
+        out["bound"] = "nvlink" if nvl_in and nvl_in / nvl_peak > nbytes / hbm else "hbm"
+        return out
+
+    ra = pass_roof("pass_a", bytes_a, t_a, NVLINK_PULL_GBS)
+    rb = pass_roof("pass_b", bytes_b, t_b, NVLINK_PUSH_GBS)
+    dom = ra if t_a >= t_b else rb
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        d = json.load(open(tp)).get(f"{wl.name}/D{D}/{args.comm if D > 1 else 'fused'}/{dom}")
+        d = json.load(open(tp)).get(f"{wl.name}/D{D}/{args.comm if D > 1 else 'fused'}/{dom['kernel']}")
         traffic = d["bytes"] if d else None
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": traffic, "peak_source": hbm_src,
-            "algorithmic_bytes_per_launch": bytes_dom, "launch_ms": t_dom,
-            "pass_a": {"bytes": bytes_a, "ms": t_a, "GBps": bytes_a / (t_a / 1e3) / 1e9},
-            "pass_b": {"bytes": bytes_b, "ms": t_b, "GBps": bytes_b / (t_b / 1e3) / 1e9},
-            "step_compulsory_frac": (owned * 28 / (ms / 1e3) / 1e9) / hbm}
+    if dom["bound"] == "nvlink":
+        roof = {"bound": "nvlink", "kernel": dom["kernel"], "achieved": dom["nvlink_GBps"],
+                "peak": dom["nvlink_peak"], "unit": "GB/s", "frac": dom["nvlink_frac"],
+                "traffic": traffic,
+                "peak_source": "measured all-to-all per-GPU in-bound NVLink (tools/p2p_bench.cu)"}
+    else:
+        roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["GBps"], "peak": hbm,
+                "unit": "GB/s", "frac": dom["hbm_frac"], "traffic": traffic, "peak_source": hbm_src}
+    roof.update({"algorithmic_bytes_per_launch": dom["bytes"], "launch_ms": dom["ms"],
+                 "pass_a": ra, "pass_b": rb,
+                 "step_compulsory_frac": (owned * 28 / (ms / 1e3) / 1e9) / hbm})
     if D > 1:
         nvl = 2 * owned * (D - 1) * 2   # bytes in per GPU: peers' grads (RS) + peers' params (AG)
         roof["nvlink"] = {"bytes_in_per_gpu": nvl, "GBps_step": nvl / (ms / 1e3) / 1e9,

@@ -15,6 +15,7 @@ for path in sys.argv[1:]:
             print("  ", line[:200])
             continue
         r, p = d["roofline"], d["phases_ms"]
-        print("  ms %.3f  %.1f Gp/s  A %.3f ms %.0f GB/s  B %.3f ms %.0f GB/s  nvl-frac %s" % (
-            d["ms_per_step"], d["value"] / 1e9, p["pass_a"], r["pass_a"]["GBps"], p["pass_b"],
-            r["pass_b"]["GBps"], r.get("nvlink", {}).get("frac_step")))
+        ra, rb = r["pass_a"], r["pass_b"]
+        print("  ms %.3f  %.1f Gp/s  A %.3f ms %.0f GB/s nvl %s  B %.3f ms %.0f GB/s nvl %s  roof %s %.3f" % (
+            d["ms_per_step"], d["value"] / 1e9, p["pass_a"], ra["GBps"], ra.get("nvlink_frac"), p["pass_b"],
+            rb["GBps"], rb.get("nvlink_frac"), r["bound"], r["frac"]))
