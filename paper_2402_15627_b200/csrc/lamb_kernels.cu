@@ -173,6 +173,96 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_a_kernel(const __grid_con
     }
 }
 
+// Pass A with a one-block-deep prefetch of the gradient words (FUSED, NS >= 2): the next
+// U-block's bf16 loads (mostly remote, ~2-3x the local latency) are issued before the current
+// block is computed, so the local m/v/w stream of the next block no longer waits behind them.
+template <int NS>
+__device__ __forceinline__ float4 sum_raw(const uint2 (&raw)[NS]) {
+    float4 s = make_float4(bf_lo(raw[0].x), bf_hi(raw[0].x), bf_lo(raw[0].y), bf_hi(raw[0].y));
+#pragma unroll
+    for (int j = 1; j < NS; ++j) {
+        s.x = __fadd_rn(s.x, bf_lo(raw[j].x));
+        s.y = __fadd_rn(s.y, bf_hi(raw[j].x));
+        s.z = __fadd_rn(s.z, bf_lo(raw[j].y));
+        s.w = __fadd_rn(s.w, bf_hi(raw[j].y));
+    }
+    return s;
+}
+
+template <int NS, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) pass_a_pf_kernel(const __grid_constant__ StepParams P) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
+    if (P.clip && P.clip->skip) return;
+    const float gs = P.clip ? P.clip->gs : P.grad_scale;
+    for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
+        const Item I = P.items[it];
+        const GroupConst& G = P.groups[I.group];
+        float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
+        float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
+        const float4* __restrict__ wp = reinterpret_cast<const float4*>(P.w + I.shard_off);
+        const int n = I.n_chunk;
+        double dw = 0.0, du = 0.0;
+        int c = lane;
+        uint2 raw[U][NS];
+        if (c + 32 * (U - 1) < n) {
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+#pragma unroll
+                for (int j = 0; j < NS; ++j)
+                    raw[k][j] = __ldcs(reinterpret_cast<const uint2*>(P.gsrc[j] + I.flat_off) + c + 32 * k);
+        }
+        for (; c + 32 * (U - 1) < n; c += 32 * U) {
+            float4 m[U], v[U], w[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                m[k] = __ldcs(mp + c + 32 * k);
+                v[k] = __ldcs(vp + c + 32 * k);
+                w[k] = __ldcs(wp + c + 32 * k);
+            }
+            const int cn = c + 32 * U;
+            const bool more = cn + 32 * (U - 1) < n;
+            uint2 nxt[U][NS];
+            if (more) {
+#pragma unroll
+                for (int k = 0; k < U; ++k)
+#pragma unroll
+                    for (int j = 0; j < NS; ++j)
+                        nxt[k][j] = __ldcs(reinterpret_cast<const uint2*>(P.gsrc[j] + I.flat_off) + cn + 32 * k);
+            }
+            float sw = 0.f, su = 0.f;
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                chunk_a(sum_raw<NS>(raw[k]), m[k], v[k], w[k], gs, G, sw, su);
+                __stcs(mp + c + 32 * k, m[k]);
+                __stcs(vp + c + 32 * k, v[k]);
+            }
+            dw += (double)sw;
+            du += (double)su;
+            if (more) {
+#pragma unroll
+                for (int k = 0; k < U; ++k)
+#pragma unroll
+                    for (int j = 0; j < NS; ++j) raw[k][j] = nxt[k][j];
+            }
+        }
+        for (; c < n; c += 32) {
+            float4 g = load_grad<NS>(P, I, 4 * (int64_t)c), m = __ldcs(mp + c), v = __ldcs(vp + c);
+            const float4 w = __ldcs(wp + c);
+            float sw = 0.f, su = 0.f;
+            chunk_a(g, m, v, w, gs, G, sw, su);
+            __stcs(mp + c, m);
+            __stcs(vp + c, v);
+            dw += (double)sw;
+            du += (double)su;
+        }
+        dw = warp_sum(dw);
+        du = warp_sum(du);
+        if (lane == 0) P.partials[it] = make_double2(dw, du);
+    }
+}
+
 // ------------------------------------------------------------ pass B
 __device__ __forceinline__ uint2 chunk_b(const float4 m, const float4 v, float4& w, float scale,
                                          const GroupConst& G) {
@@ -501,11 +591,12 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* _
 // r01 sweep (profiles/); LAMB_TUNE="ua=U,ma=M,ub=U,mb=M" overrides for tuning runs.
 struct Tune {
     int ua = 4, ma = 2, ub = 4, mb = 2;
+    int pf = 0, upf = 2;   // FUSED (NS >= 2): prefetching pass A variant and its unroll
 };
 static Tune g_tune = [] {
     Tune t;
     if (const char* e = getenv("LAMB_TUNE")) {
-        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d", &t.ua, &t.ma, &t.ub, &t.mb);
+        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d", &t.ua, &t.ma, &t.ub, &t.mb, &t.pf, &t.upf);
     }
     return t;
 }();
@@ -515,9 +606,23 @@ static cudaError_t pass_a_v(const StepParams& p, int grid, cudaStream_t s) {
     pass_a_kernel<NS, U, M><<<grid, kThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
+template <int NS, int U>
+static cudaError_t pass_a_pf(const StepParams& p, int grid, cudaStream_t s) {
+    pass_a_pf_kernel<NS, U, 2><<<grid, kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <int NS>
 static cudaError_t pass_a_ns(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
+    if constexpr (NS >= 2) {
+        if (t.pf) {
+            if constexpr (NS == 2) {   // U = 4 fits the register budget only for two sources
+                if (t.upf == 4) return pass_a_pf<NS, 4>(p, grid, s);
+            }
+            return pass_a_pf<NS, 2>(p, grid, s);
+        }
+    }
     if (t.ua == 2 && t.ma == 4) return pass_a_v<NS, 2, 4>(p, grid, s);
     if (t.ua == 2 && t.ma == 3) return pass_a_v<NS, 2, 3>(p, grid, s);
     if (t.ua == 4 && t.ma == 3) return pass_a_v<NS, 4, 3>(p, grid, s);
