@@ -211,8 +211,10 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
+        h0 = time.perf_counter()
         for t in range(Wm + 1, Wm + K + 1):
             L.step(t)
+        host_us = (time.perf_counter() - h0) / K * 1e6   # host enqueue cost per step (async)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -327,6 +329,7 @@ def main():
                        "l2": "inputs larger than L2 (fp32 state of the shard >> 126 MB)",
                        "parallelism": f"zero2-dp{world}"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "host_enqueue_us_per_step": host_us,
             "clocks": clk.summary(),
             "phases_ms": {n: float(x) for n, x in zip(lamb.PHASES, ph_mean)}}
     print(json.dumps(line), flush=True)

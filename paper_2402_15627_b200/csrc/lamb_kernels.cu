@@ -591,7 +591,7 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* _
 // r01 sweep (profiles/); LAMB_TUNE="ua=U,ma=M,ub=U,mb=M" overrides for tuning runs.
 struct Tune {
     int ua = 4, ma = 2, ub = 4, mb = 2;
-    int pf = 0, upf = 2;   // FUSED (NS >= 2): prefetching pass A variant and its unroll
+    int pf = 1, upf = 4;   // FUSED (NS >= 2): prefetching pass A (U = 4 for NS = 2, else 2; r01 sweep)
 };
 static Tune g_tune = [] {
     Tune t;

@@ -34,6 +34,12 @@ def test_parity_4gpu(mode):
     _torchrun(4, "--mode", mode)
 
 
+@pytest.mark.skipif(NGPU < 3, reason="needs >= 3 GPUs")
+def test_parity_3gpu_fused():
+    """Non-power-of-two world: Q = 128 lcm(3, 8) changes the layout, grad_scale = 1/3 is inexact."""
+    _torchrun(3, "--mode", "fused")
+
+
 @pytest.mark.skipif(NGPU < 8, reason="needs 8 GPUs")
 def test_parity_8gpu_fused():
     _torchrun(8, "--mode", "fused", "--big")
