@@ -130,13 +130,14 @@ lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors, const lam
 lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void* stream);
 
 /* COLLECTIVE.  End-to-end variant with HOST buffers: copies `host_grads` (flat bf16,
- * flat_size elements, pinned for full speed) into the grad buffer, runs lamb_step, and
- * copies the full updated bf16 param buffer back into `host_params` (flat_size elements).
- * The upload runs on an internal copy stream that waits only until the previous step has
- * released the grad buffer (so it overlaps the previous call's download): `host_grads` must
- * hold the gradients when the call is made and stay unchanged until `stream` completes.
- * `stream` completes once host_params holds the params; synchronise it before reading.
- * EINVAL: null buffers, step < 1.  ESTATE: master not set. */
+ * flat_size elements, pinned for full speed) into the grad buffer, runs the step, and copies
+ * the full updated bf16 param buffer back into `host_params` (flat_size elements).
+ * Consecutive calls form a pipeline on internal streams: the upload of step t+1 and its pass A
+ * run while step t's params are downloaded; only pass B waits for that download.  The first
+ * call is ordered after the work on `stream`; later calls are ordered among themselves (do not
+ * interleave with lamb_step without synchronising).  `host_grads` must hold the gradients when
+ * the call is made and stay unchanged until `stream` completes; `stream` completes once
+ * host_params holds the params.  EINVAL: null buffers, step < 1.  ESTATE: master not set. */
 lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_params,
                            int64_t step, void* stream);
 

@@ -63,12 +63,13 @@ struct lamb_ctx {
     float* g32 = nullptr;          // NCCL mode: reduced fp32 grad shard
     float* up32[2] = {nullptr, nullptr};   // NCCL mode: upcast staging, 2 buckets
     int64_t max_bucket = 0;
-    std::vector<cudaEvent_t> ev_rs, ev_a, ev_b, ev_up;
-    cudaEvent_t ev_start = nullptr, ev_x = nullptr, ev_done = nullptr;
+    std::vector<cudaEvent_t> ev_rs, ev_b;   // NCCL mode: per-bucket RS done / pass B done
+    cudaEvent_t ev_start = nullptr, ev_done = nullptr;
     cudaEvent_t ev_grad_free = nullptr;                  // grad buffer may be overwritten
     // lamb_step_host: copy streams and events (created on first use)
-    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-    cudaEvent_t ev_h2d = nullptr, ev_params = nullptr, ev_d2h = nullptr;
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr, work_stream = nullptr;
+    cudaEvent_t ev_h2d = nullptr, ev_params = nullptr, ev_d2h = nullptr, ev_call = nullptr;
+    cudaEvent_t pre_b_event = nullptr;   // step_impl waits on it before pass B (lamb_step_host)
     int grid_a = 0, grid_b = 0;
     int max_ctas = 0;   // SM budget of the streaming passes (0 = one full wave)
     // synth tables (device)

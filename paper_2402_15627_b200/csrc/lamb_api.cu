@@ -143,11 +143,12 @@ static void free_ctx(lamb_ctx* h) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->err_flag_host) cudaFreeHost(h->err_flag_host);
-    for (auto* vec : {&h->ev_rs, &h->ev_a, &h->ev_b, &h->ev_up, &h->tev})
+    for (auto* vec : {&h->ev_rs, &h->ev_b, &h->tev})
         for (cudaEvent_t e : *vec) cudaEventDestroy(e);
-    for (cudaEvent_t e : {h->ev_start, h->ev_x, h->ev_done, h->ev_grad_free, h->ev_h2d, h->ev_params, h->ev_d2h})
+    for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_grad_free, h->ev_h2d, h->ev_params, h->ev_d2h,
+                          h->ev_call})
         if (e) cudaEventDestroy(e);
-    for (cudaStream_t st : {h->comm_stream, h->h2d_stream, h->d2h_stream})
+    for (cudaStream_t st : {h->comm_stream, h->h2d_stream, h->d2h_stream, h->work_stream})
         if (st) cudaStreamDestroy(st);
     if (h->comm) ncclCommDestroy(h->comm);
     delete h;
@@ -381,7 +382,6 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
     h->grid_a = pass_grid(cfg->device, D, false, false, 1);
     h->grid_b = pass_grid(cfg->device, 1, false, true, D);
     CUDA_STEP(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
-    CUDA_STEP(cudaEventCreateWithFlags(&h->ev_x, cudaEventDisableTiming));
     CUDA_STEP(cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming));
     CUDA_STEP(cudaEventCreateWithFlags(&h->ev_grad_free, cudaEventDisableTiming));
     for (int j = 0; j < LAMB_MAX_RANKS; ++j) {
@@ -398,7 +398,7 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
             CUDA_STEP(dalloc(&h->up32[0], (size_t)h->max_bucket));
             CUDA_STEP(dalloc(&h->up32[1], (size_t)h->max_bucket));
             const int64_t B = p.n_buckets();
-            for (auto* vec : {&h->ev_rs, &h->ev_a, &h->ev_b, &h->ev_up}) {
+            for (auto* vec : {&h->ev_rs, &h->ev_b}) {
                 vec->resize(B);
                 for (auto& e : *vec) CUDA_STEP(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             }
@@ -549,6 +549,12 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
             if (fp.n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
         }
         mark(h, 4, s);
+        if (h->pre_b_event) {
+            // lamb_step_host: the previous step's download of the param buffer(s) must finish
+            // before pass B rewrites them — on every rank, since pass B stores into peers
+            CUDA_TRY(h, cudaStreamWaitEvent(s, h->pre_b_event, 0));
+            if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+        }
         const bool push = fused && !defer_ag;
         for (int j = 0; j < D; ++j) sp.pdst[j] = push ? h->peer_param[j] : h->param;
         LAUNCH(h, launch_pass_b(sp, push ? D : 1, grid_b, s));
@@ -606,6 +612,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         if (fp.n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
     }
     mark(h, 4, s);
+    if (h->pre_b_event) CUDA_TRY(h, cudaStreamWaitEvent(s, h->pre_b_event, 0));   // see above
     sp.pdst[0] = h->param;
     for (int64_t b = b0; b < b1; ++b) {
         sp.item_begin = h->bucket_item_begin[b];
@@ -694,11 +701,14 @@ extern "C" lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream
 
 extern "C" lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_params,
                                       int64_t step, void* stream) {
-    // Pipeline across consecutive calls: the H2D of this step's grads runs on its own copy
-    // stream as soon as the previous step released the grad buffer (ev_grad_free), i.e.
-    // concurrently with the previous step's D2H of params on the other copy engine.  The
-    // step itself is ordered on `stream` after the upload; `stream` completes once the
-    // params are in host_params.
+    // Three-stage pipeline across consecutive calls, on internal streams:
+    //   copy-in  : H2D of this step's grads, as soon as the previous step released the grad
+    //              buffer (ev_grad_free) — concurrent with the previous step's download;
+    //   work     : the LAMB step; only pass B waits for the previous download (it rewrites the
+    //              param buffers), so pass A overlaps it too;
+    //   copy-out : D2H of the updated params.
+    // `stream` gets a dependency on the download: it completes once host_params holds the
+    // params.  The first call also orders the pipeline after the work already on `stream`.
     if (!h || !host_grads || !host_params) return fail(h, LAMB_EINVAL, "null argument");
     if (step < 1) return fail(h, LAMB_EINVAL, "step must be >= 1");
     if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step_host before lamb_set_master / lamb_synth_init");
@@ -707,18 +717,25 @@ extern "C" lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint
     if (!h->h2d_stream) {
         CUDA_TRY(h, cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
         CUDA_TRY(h, cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
+        CUDA_TRY(h, cudaStreamCreateWithFlags(&h->work_stream, cudaStreamNonBlocking));
         CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_h2d, cudaEventDisableTiming));
         CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_params, cudaEventDisableTiming));
         CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_d2h, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_call, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventRecord(h->ev_call, s));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->work_stream, h->ev_call, 0));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_call, 0));
     }
     const size_t bytes = (size_t)h->plan.flat_size * 2;
     CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_grad_free, 0));
     CUDA_TRY(h, cudaMemcpyAsync(h->grad, host_grads, bytes, cudaMemcpyHostToDevice, h->h2d_stream));
     CUDA_TRY(h, cudaEventRecord(h->ev_h2d, h->h2d_stream));
-    CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_h2d, 0));
-    lamb_status st = lamb_step(h, nullptr, step, stream);
+    CUDA_TRY(h, cudaStreamWaitEvent(h->work_stream, h->ev_h2d, 0));
+    h->pre_b_event = h->ev_d2h;   // previous download (a never-recorded event is a no-op)
+    lamb_status st = lamb_step(h, nullptr, step, h->work_stream);
+    h->pre_b_event = nullptr;
     if (st != LAMB_OK) return st;
-    CUDA_TRY(h, cudaEventRecord(h->ev_params, s));
+    CUDA_TRY(h, cudaEventRecord(h->ev_params, h->work_stream));
     CUDA_TRY(h, cudaStreamWaitEvent(h->d2h_stream, h->ev_params, 0));
     CUDA_TRY(h, cudaMemcpyAsync(host_params, h->param, bytes, cudaMemcpyDeviceToHost, h->d2h_stream));
     CUDA_TRY(h, cudaEventRecord(h->ev_d2h, h->d2h_stream));
