@@ -145,6 +145,43 @@ def bucket_case(world, rank, local, mode):
         print(f"[ok] per-bucket stepping D={world} mode={mode} buckets={nb} == lamb_step (bitwise)", flush=True)
 
 
+def host_case(world, rank, local, mode):
+    """lamb_step_host pipeline (upload / step / download on internal streams, pass B gated on
+    every rank's previous download) == lamb_step on device grads, bitwise, at D ranks."""
+    from paper_2402_15627_b200 import lamb
+    rng = np.random.default_rng(103)
+    tensors = W.random_table(rng, 30, max_numel=6000, p_big=0.2, big=40_000)
+    wl = W.Workload("hostd", 74, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    mk = lambda: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
+                           device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD)
+    A, B = mk(), mk()
+    for L in (A, B):
+        L.synth_init(spec, wl.seed)
+    n = A.plan.flat_size
+    hg = [torch.empty(n, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    hp = [torch.empty(n, dtype=torch.bfloat16).pin_memory() for _ in range(3)]
+    for t in range(1, 4):
+        A.synth_grads(spec, wl.seed, rank + 1, t)
+        hg[t - 1].copy_(A.grad_buffer())
+    torch.cuda.synchronize()
+    for t in range(1, 4):
+        A.step_host(hg[t - 1], hp[t - 1], t)
+    torch.cuda.synchronize()
+    for t in range(1, 4):
+        B.synth_grads(spec, wl.seed, rank + 1, t)
+        B.step(t)
+        torch.cuda.synchronize()
+        assert torch.equal(hp[t - 1].view(torch.int16), B.param_buffer().cpu().view(torch.int16)), t
+    for k in (2, 3, 4):
+        assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32)), k
+    A.close()
+    B.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] lamb_step_host pipeline D={world} mode={mode} == lamb_step (bitwise)", flush=True)
+
+
 def ckpt_case(world, rank, local, mode):
     """Checkpoint saved by D ranks; reloaded (a) by D ranks with another bucket cap and
     (b) by rank 0 alone at D = 1 (reshard); both continue and must match the oracle."""
@@ -229,6 +266,7 @@ def main():
     ckpt_case(world, rank, local, mode)
     clip_case(world, rank, local, mode)
     bucket_case(world, rank, local, mode)
+    host_case(world, rank, local, mode)
     if a.big:
         wl = W.gpt_1p3b()
         ids = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 289, 290]
