@@ -159,6 +159,14 @@ lamb_status lamb_step_bucket(lamb_t h, int64_t bucket, int64_t step, int32_t fla
  * 0 = one full wave, the default) so that a concurrently running compute stream keeps the
  * remaining SMs.  Applies to subsequent lamb_step / lamb_step_bucket calls.  EINVAL: < 0. */
 lamb_status lamb_set_max_ctas(lamb_t h, int32_t max_ctas);
+/* Splits `device`'s SMs into two green contexts (CUDA 12.4+ driver API): lamb_sms SMs (rounded
+ * up to the hardware's SM-group granularity; the count is returned in *got_sms) and the rest,
+ * and returns one non-blocking stream in each.  Kernels launched into a stream run only on its
+ * SMs — the hard partition that overlapping lamb_step_bucket with compute needs (a cuBLAS
+ * SM-count target is only a heuristic).  Streams live until process exit.
+ * EINVAL: bad arguments.  EUNSUPPORTED: driver without green contexts. */
+lamb_status lamb_sm_partition(int32_t device, int32_t lamb_sms, void** lamb_stream, void** compute_stream,
+                              int32_t* got_sms);
 /* Deferred all-gather of one bucket's bf16 params (FUSED: NVLink pull of the D-1 peer slices;
  * NCCL: ncclAllGather, COLLECTIVE).  No-op at D = 1. */
 lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream);

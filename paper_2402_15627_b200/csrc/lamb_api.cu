@@ -11,6 +11,7 @@
 // overlapped with pass A of earlier buckets; ncclAllGather(fp64) of straddler rows;
 // per-bucket ncclAllGather(bf16) of params overlapped with pass B of later buckets.
 // D = 1: pass A -> finalize -> pass B.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -817,6 +818,57 @@ extern "C" lamb_status lamb_set_lr(lamb_t h, int32_t group, float lr) {
     if (group < 0 || group >= (int32_t)h->groups.size()) return fail(h, LAMB_EINVAL, "group out of range");
     if (!(lr >= 0.f)) return fail(h, LAMB_EINVAL, "lr must be >= 0");
     h->groups[group].lr = lr;
+    return LAMB_OK;
+}
+
+// ------------------------------------------------------------------ SM partition (NEXT #2)
+// Green contexts (CUDA 12.4+ driver API), resolved through cudaGetDriverEntryPoint so the
+// library carries no link-time dependency on libcuda (it still loads on a driverless host).
+template <typename F>
+static bool driver_fn(const char* name, F* out) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return false;
+    *out = reinterpret_cast<F>(fn);
+    return true;
+}
+
+extern "C" lamb_status lamb_sm_partition(int32_t device, int32_t lamb_sms, void** lamb_stream,
+                                         void** compute_stream, int32_t* got_sms) {
+    if (!lamb_stream || !compute_stream || lamb_sms < 1) return fail(nullptr, LAMB_EINVAL, "bad arguments");
+    CUresult (*getDev)(CUdevice*, int) = nullptr;
+    CUresult (*getRes)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+    CUresult (*split)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*, unsigned int,
+                      unsigned int) = nullptr;
+    CUresult (*genDesc)(CUdevResourceDesc*, CUdevResource*, unsigned int) = nullptr;
+    CUresult (*gcCreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int) = nullptr;
+    CUresult (*gcStream)(CUstream*, CUgreenCtx, unsigned int, int) = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess || cudaFree(nullptr) != cudaSuccess)
+        return fail(nullptr, LAMB_ECUDA, "cannot initialise the device");
+    if (!driver_fn("cuDeviceGet", &getDev) || !driver_fn("cuDeviceGetDevResource", &getRes) ||
+        !driver_fn("cuDevSmResourceSplitByCount", &split) || !driver_fn("cuDevResourceGenerateDesc", &genDesc) ||
+        !driver_fn("cuGreenCtxCreate", &gcCreate) || !driver_fn("cuGreenCtxStreamCreate", &gcStream))
+        return fail(nullptr, LAMB_EUNSUPPORTED, "green contexts are not available from this driver");
+    CUdevice dev;
+    CUdevResource all, part, rest;
+    unsigned int ng = 1;
+    if (getDev(&dev, device) != CUDA_SUCCESS || getRes(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+        split(&part, &ng, &all, &rest, 0, (unsigned)lamb_sms) != CUDA_SUCCESS || ng != 1)
+        return fail(nullptr, LAMB_EUNSUPPORTED, "cannot split the SMs");
+    CUdevResourceDesc d1, d2;
+    CUgreenCtx g1, g2;
+    CUstream s1, s2;
+    if (genDesc(&d1, &part, 1) != CUDA_SUCCESS || genDesc(&d2, &rest, 1) != CUDA_SUCCESS ||
+        gcCreate(&g1, d1, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        gcCreate(&g2, d2, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+        gcStream(&s1, g1, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS ||
+        gcStream(&s2, g2, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+        return fail(nullptr, LAMB_EUNSUPPORTED, "cannot create the green contexts");
+    *lamb_stream = s1;
+    *compute_stream = s2;
+    if (got_sms) *got_sms = (int32_t)part.sm.smCount;
     return LAMB_OK;
 }
 

@@ -88,6 +88,8 @@ _SIGS = {
     "lamb_step_bucket": (_st, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _vp]),
     "lamb_gather_bucket": (_st, [_vp, ctypes.c_int64, _vp]),
     "lamb_set_max_ctas": (_st, [_vp, ctypes.c_int32]),
+    "lamb_sm_partition": (_st, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                ctypes.POINTER(ctypes.c_int32)]),
     "lamb_destroy": (None, [_vp]),
     "lamb_query_plan": (_st, [_vp, ctypes.POINTER(lamb_plan_view)]),
     "lamb_buffer": (_st, [_vp, ctypes.c_int32, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64)]),
@@ -179,6 +181,13 @@ def device_philox(ctr: Sequence[int], key: Sequence[int]) -> List[int]:
     o = (ctypes.c_uint32 * 4)()
     check(lamb_synth_philox(c, k, o))
     return list(o)
+
+
+def sm_partition(device: int, lamb_sms: int):
+    """(lamb_stream_ptr, compute_stream_ptr, sms) — two green-context streams (see lamb.h)."""
+    a, b, n = _vp(), _vp(), ctypes.c_int32()
+    check(lamb_sm_partition(device, lamb_sms, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
+    return a.value, b.value, n.value
 
 
 def get_unique_id() -> bytes:

@@ -33,7 +33,9 @@ ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU per ite
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--ctas", default="0,74,37", help="SM budgets (max CTAs) to try in overlap mode")
-ap.add_argument("--carveouts", default="8,16,32",
+ap.add_argument("--green", default="16,32,48",
+                help="green-context SM partitions to try (LAMB gets these SMs, the GEMMs the rest)")
+ap.add_argument("--carveouts", default="",
                 help="cuBLAS SM carve-outs to try (LAMB gets max_ctas = 2 x carve-out)")
 ap.add_argument("--cap", type=int, default=0, help="bucket cap (0 = the workload's)")
 ap.add_argument("--K", type=int, default=2048, help="synthetic GEMM size [tokens,K]x[K,K]")
@@ -68,7 +70,7 @@ reps_f = [max(1, round(2.0 * P * a.tokens / gemm_flops)) for P in params_b]
 
 def gemms(n):
     for _ in range(n):
-        torch.matmul(X, Wm, out=Y)
+        torch.matmul(X, Wm, out=Y)   # on the current stream (set by iteration)
 
 
 comp = torch.cuda.current_stream()
@@ -79,9 +81,10 @@ ev_ls_done = torch.cuda.Event()
 step = [0]
 
 
-def iteration(mode):
+def iteration(mode, comp=comp, ls=ls):
     step[0] += 1
     t = step[0]
+    torch.cuda.set_stream(comp)
     if mode == "overlap":
         # forward: gathers issued in bucket order (the first is the prefetch), each forward waits
         with torch.cuda.stream(ls):
@@ -110,16 +113,16 @@ def iteration(mode):
                 L.step_bucket(b, t, stream=comp)
 
 
-def timed(mode):
+def timed(mode, comp=comp, ls=ls):
     for _ in range(a.warmup):
-        iteration(mode)
+        iteration(mode, comp, ls)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(comp)
     for _ in range(a.iters):
-        iteration(mode)
+        iteration(mode, comp, ls)
     e1.record(comp)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.iters
@@ -144,6 +147,15 @@ for k in [int(x) for x in a.carveouts.split(",") if x]:
     over[f"carveout{k}"] = timed("overlap")
     res[f"compute_carveout{k}"] = timed("compute")
     torch._C._set_sm_carveout_experimental(0)
+torch.cuda.set_stream(comp)
+for k in [int(x) for x in a.green.split(",") if x]:
+    # hard SM partition: LAMB on k SMs, the GEMMs on the other 148 - k
+    lp, cpp, got = lamb.sm_partition(local, k)
+    gls, gcs = torch.cuda.ExternalStream(lp), torch.cuda.ExternalStream(cpp)
+    L.set_max_ctas(2 * got)
+    over[f"green{got}"] = timed("overlap", gcs, gls)
+    res[f"compute_green{got}"] = timed("compute", gcs, gls)
+    torch.cuda.set_stream(comp)
 L.set_max_ctas(0)
 res["compute"] = min(res["compute"], timed("compute"))
 if rank == 0:
@@ -155,6 +167,7 @@ if rank == 0:
                       "ms_compute": res["compute"], "ms_serial": res["serial"],
                       "ms_serial_buckets": res["serial_buckets"], "K": K, "cap": a.cap or wl.cap,
                       "ms_compute_with_carveout": {k: v for k, v in res.items() if k.startswith("compute_carveout")},
+                      "ms_compute_on_partition": {k: v for k, v in res.items() if k.startswith("compute_green")},
                       "ms_overlap_by_max_ctas": over, "best_max_ctas": best, "ms_overlap": over[best],
                       "exposed_ms_serial": exposed_serial, "exposed_ms_overlap": exposed_overlap,
                       "hidden_frac": 1.0 - exposed_overlap / exposed_serial if exposed_serial > 0 else None}))
