@@ -366,3 +366,35 @@ def test_step_bucket_equals_step(lamb, defer):
     assert e.value.status == lamb.LAMB_EUNSUPPORTED
     A.close()
     B.close()
+
+
+def test_results_independent_of_grid_and_sm_partition(lamb):
+    """Determinism does not depend on the launch configuration: per-item partials are fixed
+    reductions whatever warp runs the item, so any SM budget (lamb_set_max_ctas) or a green-
+    context SM partition gives bit-identical state."""
+    rng = np.random.default_rng(61)
+    tensors = W.random_table(rng, 40, max_numel=20000, p_big=0.2, big=200_000)
+    wl = W.Workload("grid", 96, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    outs = []
+    for mode in ("full", "ctas7", "ctas148", "green"):
+        L = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=100_000)
+        L.synth_init(spec, wl.seed)
+        stream = None
+        if mode.startswith("ctas"):
+            L.set_max_ctas(int(mode[4:]))
+        if mode == "green":
+            lp, _, got = lamb.sm_partition(0, 16)
+            assert 16 <= got < 148
+            stream = torch.cuda.ExternalStream(lp)
+            L.set_max_ctas(2 * got)
+        for t in (1, 2):
+            L.synth_grads(spec, wl.seed, 1, t)
+            L.step(t, stream=stream)
+        torch.cuda.synchronize()
+        outs.append([L.get_state(k).view(np.uint32) for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V)]
+                    + [L.param_buffer().view(torch.int16).cpu().numpy()])
+        L.close()
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
