@@ -113,8 +113,12 @@ lamb_status lamb_get_unique_id(uint8_t id[LAMB_UNIQUE_ID_BYTES]);
  * fp32 w/m/v shards), creates the NCCL communicator and, in LAMB_COMM_FUSED, maps every
  * peer's grad/param/exchange buffers over NVLink (CUDA IPC).  `id` may be NULL when D = 1.
  * EINVAL: see lamb_plan_create, n_groups not in [1, LAMB_MAX_GROUPS], group out of range,
- * bad hyper-parameters, reserved != 0.  ENOMEM, ECUDA, ENCCL, EUNSUPPORTED (device not
- * sm_100, or peers not NVLink-reachable in FUSED mode). */
+ * bad hyper-parameters, reserved != 0, or (D > 1) another rank passed a different table /
+ * config (a hash is all-gathered and compared; every rank fails).  ENOMEM, ECUDA, ENCCL,
+ * EUNSUPPORTED (device not sm_100, or peers not NVLink-reachable in FUSED mode).
+ * Failure detection: every cross-GPU wait is bounded by LAMB_BARRIER_TIMEOUT_MS (environment,
+ * default 30000); a peer that does not arrive makes the next call return LAMB_ECUDA, after
+ * which the handle must be destroyed. */
 lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors, const lamb_group* groups,
                         int32_t n_groups, const lamb_config* cfg,
                         const uint8_t id[LAMB_UNIQUE_ID_BYTES], lamb_t* out);

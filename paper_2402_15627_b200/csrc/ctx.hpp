@@ -72,6 +72,7 @@ struct lamb_ctx {
     cudaEvent_t pre_b_event = nullptr;   // step_impl waits on it before pass B (lamb_step_host)
     int grid_a = 0, grid_b = 0;
     int max_ctas = 0;   // SM budget of the streaming passes (0 = one full wave)
+    uint64_t barrier_timeout_ns = 30000000000ull;   // LAMB_BARRIER_TIMEOUT_MS at create
     // synth tables (device)
     int64_t *d_tensor_off = nullptr, *d_numel = nullptr, *d_shard_base = nullptr,
             *d_bucket_base = nullptr, *d_bucket_slice = nullptr;

@@ -16,6 +16,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -250,6 +251,32 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
     ncclUniqueId u;
     memcpy(&u, id, sizeof(u));
     NCCL_TRY(h, ncclCommInitRank(&h->comm, D, u, r));
+    {
+        // collective-misuse check: every rank must pass the same tables and config (except
+        // rank/device) — a 64-bit FNV-1a hash of them is all-gathered and compared
+        uint64_t hv = 1469598103934665603ull;
+        auto mix = [&](const void* data, size_t n) {
+            const unsigned char* b = static_cast<const unsigned char*>(data);
+            for (size_t i = 0; i < n; ++i) hv = (hv ^ b[i]) * 1099511628211ull;
+        };
+        mix(h->plan.numel.data(), h->plan.numel.size() * 8);
+        mix(h->plan.group.data(), h->plan.group.size() * 4);
+        mix(h->groups.data(), h->groups.size() * sizeof(lamb_group));
+        const int64_t cfgv[4] = {h->cfg.world_size, h->cfg.comm_mode, h->plan.cap, (int64_t)h->cfg.flags};
+        mix(cfgv, sizeof(cfgv));
+        mix(&h->cfg.grad_scale, sizeof(float));
+        uint64_t* dh = nullptr;
+        CUDA_TRY(h, cudaMalloc(&dh, 8 * (D + 1)));
+        CUDA_TRY(h, cudaMemcpy(dh + D, &hv, 8, cudaMemcpyHostToDevice));
+        NCCL_TRY(h, ncclAllGather(dh + D, dh, 1, ncclUint64, h->comm, 0));
+        std::vector<uint64_t> all(D);
+        CUDA_TRY(h, cudaMemcpy(all.data(), dh, 8 * D, cudaMemcpyDeviceToHost));
+        cudaFree(dh);
+        for (int j = 0; j < D; ++j)
+            if (all[j] != hv)
+                return fail(h, LAMB_EINVAL, "lamb_create: rank " + std::to_string(j) +
+                                                " passed a different tensor/group table or config");
+    }
     for (int j = 0; j < D; ++j) {
         h->peer_grad[j] = h->grad;
         h->peer_param[j] = h->param;
@@ -312,6 +339,12 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
 
     auto* h = new lamb_ctx();
     h->cfg = *cfg;
+    {
+        // failure detection: bound on every cross-GPU wait (a missing peer must not hang the GPU)
+        const char* e = getenv("LAMB_BARRIER_TIMEOUT_MS");
+        const long ms = e ? atol(e) : 30000;
+        h->barrier_timeout_ns = (uint64_t)(ms > 0 ? ms : 30000) * 1000000ull;
+    }
     h->device = cfg->device;
     h->groups.assign(groups, groups + n_groups);
     if (h->cfg.grad_scale == 0.f) h->cfg.grad_scale = 1.0f / (float)cfg->world_size;
@@ -519,7 +552,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         // ---------------- D = 1 or FUSED
         uint64_t* flags[LAMB_MAX_RANKS];
         for (int j = 0; j < D; ++j) flags[j] = h->flags(j);
-        if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+        if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
         mark(h, 1, s);
         for (int j = 0; j < D; ++j)
             sp.gsrc[j] = fused ? h->peer_grad[j] : (grads ? (const __nv_bfloat16*)grads : h->grad);
@@ -529,7 +562,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
             LAUNCH(h, launch_grad_stats(sp, D, fused, grid_a, s));
             LAUNCH(h, launch_clip_finalize(cp, s));
             if (fused) {
-                LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+                LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
                 LAUNCH(h, launch_clip_combine(cp, s));
                 sp.g32 = h->g32;
                 LAUNCH(h, launch_pass_a(sp, 0, true, grid_a, s));
@@ -546,7 +579,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         mark(h, 3, s);
         if (fused && strad) {
             // straddler rows travel through peer memory: barrier, then sum in rank order
-            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
             if (fp.n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
         }
         mark(h, 4, s);
@@ -554,7 +587,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
             // lamb_step_host: the previous step's download of the param buffer(s) must finish
             // before pass B rewrites them — on every rank, since pass B stores into peers
             CUDA_TRY(h, cudaStreamWaitEvent(s, h->pre_b_event, 0));
-            if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+            if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
         }
         const bool push = fused && !defer_ag;
         for (int j = 0; j < D; ++j) sp.pdst[j] = push ? h->peer_param[j] : h->param;
@@ -562,7 +595,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         mark(h, 5, s);
         if (fused) {
             // params complete everywhere, and every rank finished reading this rank's grads
-            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s));
+            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
             CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));
         }
         mark(h, 6, s);

@@ -529,7 +529,7 @@ struct BarrierArgs {
     uint64_t* flags[LAMB_MAX_RANKS];
 };
 __global__ void barrier_kernel_v(const __grid_constant__ BarrierArgs A, uint64_t* epoch, int rank,
-                                 int world, int* err) {
+                                 int world, int* err, uint64_t timeout_ns) {
     __shared__ uint64_t e;
     if (threadIdx.x == 0) {
         e = *epoch + 1;
@@ -542,7 +542,7 @@ __global__ void barrier_kernel_v(const __grid_constant__ BarrierArgs A, uint64_t
         st_release_sys(A.flags[j] + rank, e);
         const uint64_t t0 = globaltimer();
         while (ld_acquire_sys(A.flags[rank] + j) < e) {
-            if (globaltimer() - t0 > 30ull * 1000000000ull) {
+            if (globaltimer() - t0 > timeout_ns) {
                 atomicExch(err, 1);
                 break;
             }
@@ -757,10 +757,10 @@ cudaError_t launch_finalize_straddlers(const FinalizeParams& p, cudaStream_t s) 
 }
 
 cudaError_t launch_barrier(uint64_t* const* flags, uint64_t* epoch, int rank, int world,
-                           int* err_flag, cudaStream_t s) {
+                           int* err_flag, cudaStream_t s, uint64_t timeout_ns) {
     BarrierArgs a;
     for (int j = 0; j < LAMB_MAX_RANKS; ++j) a.flags[j] = j < world ? flags[j] : nullptr;
-    barrier_kernel_v<<<1, 32, 0, s>>>(a, epoch, rank, world, err_flag);
+    barrier_kernel_v<<<1, 32, 0, s>>>(a, epoch, rank, world, err_flag, timeout_ns);
     return cudaGetLastError();
 }
 

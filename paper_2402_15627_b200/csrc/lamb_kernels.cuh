@@ -116,7 +116,7 @@ cudaError_t launch_clip_combine(const ClipParams& p, cudaStream_t s);
 cudaError_t launch_finalize_segments(const FinalizeParams& p, cudaStream_t s);
 cudaError_t launch_finalize_straddlers(const FinalizeParams& p, cudaStream_t s);
 cudaError_t launch_barrier(uint64_t* const* flags, uint64_t* epoch, int rank, int world,
-                           int* err_flag, cudaStream_t s);
+                           int* err_flag, cudaStream_t s, uint64_t timeout_ns);
 cudaError_t launch_gather(const __nv_bfloat16* const* peers, __nv_bfloat16* dst, int64_t base, int64_t slice,
                           int world, int rank, cudaStream_t s);
 cudaError_t launch_upcast_bf16(const __nv_bfloat16* src, float* dst, int64_t n, cudaStream_t s);

@@ -228,6 +228,41 @@ def ckpt_case(world, rank, local, mode):
     dist.barrier()
 
 
+def failure_case(world, rank, local, mode):
+    """Failure detection: (1) a rank passing a different table makes lamb_create fail on every
+    rank; (2) in FUSED mode a rank that skips a step makes the others' barriers time out
+    (LAMB_BARRIER_TIMEOUT_MS) and their next call report LAMB_ECUDA — no hang."""
+    from paper_2402_15627_b200 import lamb
+    wl = W.toy()
+    tensors = [(t.numel, t.group) for t in wl.tensors]
+    bad = tensors if rank == 0 else tensors[:-1] + [(tensors[-1][0] + 8, tensors[-1][1])]
+    try:
+        lamb.Lamb(bad, wl.groups, world_size=world, rank=rank, device=local, comm_mode=mode, pg=dist.group.WORLD)
+        raise AssertionError("mismatched tables were accepted")
+    except lamb.LambError as e:
+        assert e.status == lamb.LAMB_EINVAL and "different" in str(e), str(e)
+    dist.barrier()
+    if mode == lamb.LAMB_COMM_FUSED:
+        L = lamb.Lamb(tensors, wl.groups, world_size=world, rank=rank, device=local, comm_mode=mode,
+                      pg=dist.group.WORLD)
+        L.synth_init(spec_of(wl), wl.seed)
+        L.step(1)
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:                 # rank 0 steps alone: its barriers give up after the timeout
+            L.step(2)
+            torch.cuda.synchronize()
+            try:
+                L.step(3)
+                raise AssertionError("missing peer not detected")
+            except lamb.LambError as e:
+                assert e.status == lamb.LAMB_ECUDA and "timed out" in str(e), str(e)
+        dist.barrier()
+        L.close()
+    if rank == 0:
+        print(f"[ok] failure detection D={world} mode={mode} (table mismatch, missing peer)", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mode", default="fused", choices=["fused", "nccl"])
@@ -267,6 +302,8 @@ def main():
     clip_case(world, rank, local, mode)
     bucket_case(world, rank, local, mode)
     host_case(world, rank, local, mode)
+    os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"
+    failure_case(world, rank, local, mode)
     if a.big:
         wl = W.gpt_1p3b()
         ids = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 289, 290]
