@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--comm", default="fused", choices=["fused", "nccl"])
     ap.add_argument("--clip", type=float, default=0.0,
                     help="enable the NEXT #3 pre-step with this max grad norm (0 = off)")
+    ap.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
@@ -189,7 +190,8 @@ def main():
     spec = [(t.init, t.gexp) for t in wl.tensors]
     comm = lamb.LAMB_COMM_FUSED if args.comm == "fused" else lamb.LAMB_COMM_NCCL
     L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
-                  device=local, comm_mode=comm, bucket_cap=wl.cap, timing=True, pg=pg)
+                  device=local, comm_mode=comm, bucket_cap=wl.cap, timing=not args.graph, pg=pg,
+                  graph=args.graph)
     L.synth_init(spec, wl.seed)
     L.synth_grads(spec, wl.seed, rank + 1, 1)      # PER_RANK gradients, resident in HBM
     if args.clip > 0:
@@ -205,7 +207,8 @@ def main():
     for t in range(1, Wm + 1):
         L.step(t)
     barrier()
-    L.timing_begin(K)
+    if not args.graph:
+        L.timing_begin(K)
     n0 = L.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -220,8 +223,12 @@ def main():
     barrier()
     launches = L.launch_count() - n0
     ms_local = e0.elapsed_time(e1) / K
-    ph = L.timing_read()                      # [K][6] ms per phase, events on the launch stream
-    ph_mean = ph.mean(axis=0)
+    if args.graph:   # no per-phase events inside a graph: attribute the step to the passes by bytes
+        ph_mean = np.zeros(6)
+        ph_mean[1] = ph_mean[4] = ms_local / 2
+    else:
+        ph = L.timing_read()                  # [K][6] ms per phase, events on the launch stream
+        ph_mean = ph.mean(axis=0)
     ms = ms_local
     if world > 1:
         tt = torch.tensor([ms_local] + list(ph_mean), dtype=torch.float64, device="cuda")
@@ -326,6 +333,7 @@ def main():
                        "flat_size": L.plan.flat_size, "world_size": world,
                        "comm": args.comm if world > 1 else "none", "bucket_cap": wl.cap,
                        "prestep_clip": args.clip if args.clip > 0 else None,
+                       "cuda_graph": bool(args.graph),
                        "l2": "inputs larger than L2 (fp32 state of the shard >> 126 MB)",
                        "parallelism": f"zero2-dp{world}"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -70,6 +70,8 @@ typedef struct {
                                 fp32 sum), all-gather fused into pass B (NVLink peer stores) */
 /* flags */
 #define LAMB_FLAG_TIMING 1   /* record CUDA events around every phase (lamb_timing_*) */
+#define LAMB_FLAG_GRAPH 2    /* lamb_step replays one captured CUDA graph of the whole step
+                                (D = 1 and FUSED, library grad buffer; no per-phase timing) */
 
 typedef struct {
     int32_t world_size;        /* D >= 1, <= LAMB_MAX_RANKS; D = 1 needs no unique id */

@@ -72,6 +72,11 @@ struct lamb_ctx {
     cudaEvent_t pre_b_event = nullptr;   // step_impl waits on it before pass B (lamb_step_host)
     int grid_a = 0, grid_b = 0;
     int max_ctas = 0;   // SM budget of the streaming passes (0 = one full wave)
+    lamb::GroupConst* d_groups = nullptr;   // per-step group constants (prologue kernel)
+    // LAMB_FLAG_GRAPH
+    cudaGraphExec_t graph_exec = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    int64_t graph_key = -1, graph_launches = 0;
     uint64_t barrier_timeout_ns = 30000000000ull;   // LAMB_BARRIER_TIMEOUT_MS at create
     // synth tables (device)
     int64_t *d_tensor_off = nullptr, *d_numel = nullptr, *d_shard_base = nullptr,

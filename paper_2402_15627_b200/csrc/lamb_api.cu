@@ -140,17 +140,18 @@ static void free_ctx(lamb_ctx* h) {
     }
     void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->partials, h->segs, h->scale,
                     h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
-                    h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_clip_blocks, h->d_tensor_off, h->d_numel,
+                    h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_clip_blocks, h->d_groups, h->d_tensor_off, h->d_numel,
                     h->d_shard_base, h->d_bucket_base, h->d_bucket_slice};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->err_flag_host) cudaFreeHost(h->err_flag_host);
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
     for (auto* vec : {&h->ev_rs, &h->ev_b, &h->tev})
         for (cudaEvent_t e : *vec) cudaEventDestroy(e);
     for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_grad_free, h->ev_h2d, h->ev_params, h->ev_d2h,
                           h->ev_call})
         if (e) cudaEventDestroy(e);
-    for (cudaStream_t st : {h->comm_stream, h->h2d_stream, h->d2h_stream, h->work_stream})
+    for (cudaStream_t st : {h->comm_stream, h->h2d_stream, h->d2h_stream, h->work_stream, h->cap_stream})
         if (st) cudaStreamDestroy(st);
     if (h->comm) ncclCommDestroy(h->comm);
     delete h;
@@ -408,6 +409,7 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
     CUDA_STEP(dalloc(&h->sync, h->sync_bytes));
     CUDA_STEP(cudaMemset(h->sync, 0, h->sync_bytes));
     CUDA_STEP(dalloc(&h->d_clip, 1));
+    CUDA_STEP(dalloc(&h->d_groups, LAMB_MAX_GROUPS));
     CUDA_STEP(dalloc(&h->d_clip_blocks, lamb::kClipBlocksMax));
     CUDA_STEP(cudaMemset(h->d_clip, 0, sizeof(lamb::ClipState)));
     CUDA_STEP(cudaHostAlloc(&h->err_flag_host, sizeof(int), cudaHostAllocMapped));
@@ -505,7 +507,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     sp.v = h->v;
     sp.partials = h->partials;
     sp.scale = h->scale;
-    group_consts(h, t, sp.groups);
+    sp.groups = h->d_groups;
     FinalizeParams fp;
     memset(&fp, 0, sizeof(fp));
     fp.segs = h->segs + h->bucket_seg_begin[b0];
@@ -523,7 +525,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     fp.strad_group = h->strad_group + h->bucket_strad_begin[b0];
     fp.n_local_strad = (int32_t)(h->bucket_strad_begin[b1] - h->bucket_strad_begin[b0]);
     fp.xbuf = h->xbuf(-1);
-    memcpy(fp.groups, sp.groups, sizeof(sp.groups));
+    fp.groups = h->d_groups;
     const bool pre = h->prestep();
     lamb::ClipParams cp;
     memset(&cp, 0, sizeof(cp));
@@ -680,6 +682,47 @@ static lamb_status check_async(lamb_ctx* h) {
     return LAMB_OK;
 }
 
+// Per-step group constants (bias corrections for this t, current lr) -> device table.
+static lamb_status prologue(lamb_ctx* h, int64_t t, cudaStream_t s) {
+    lamb::GroupTable T;
+    memset(&T, 0, sizeof(T));
+    group_consts(h, t, T.g);
+    LAUNCH(h, lamb::launch_prologue(T, (int)h->groups.size(), h->d_groups, s));
+    return LAMB_OK;
+}
+
+// LAMB_FLAG_GRAPH: the whole step (everything after the prologue) captured once into a CUDA
+// graph and replayed; re-captured when a setting that changes the launch sequence changes.
+static lamb_status graph_step(lamb_ctx* h, cudaStream_t s) {
+    const int64_t key = (h->prestep() ? 1 : 0) | ((int64_t)h->max_ctas << 1);
+    if (!h->graph_exec || key != h->graph_key) {
+        if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+        h->graph_exec = nullptr;
+        if (!h->cap_stream) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+        if (h->prestep() && h->cfg.world_size > 1 && !h->g32)   // no allocation inside a capture
+            CUDA_TRY(h, dalloc(&h->g32, (size_t)h->plan.shard_size));
+        const int32_t t_max = h->t_max;
+        h->t_max = 0;   // no per-phase events inside the graph
+        const int64_t l0 = h->launches;
+        CUDA_TRY(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+        lamb_status st = step_impl(h, nullptr, 1, h->cap_stream, 0, h->plan.n_buckets(), false);
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(h->cap_stream, &g);
+        h->t_max = t_max;
+        if (st != LAMB_OK) return st;
+        if (ce != cudaSuccess) return fail(h, LAMB_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        h->graph_launches = h->launches - l0;
+        h->launches = l0;
+        ce = cudaGraphInstantiate(&h->graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) return fail(h, LAMB_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+        h->graph_key = key;
+    }
+    CUDA_TRY(h, cudaGraphLaunch(h->graph_exec, s));
+    h->launches += h->graph_launches;
+    return LAMB_OK;
+}
+
 extern "C" lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void* stream) {
     if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
     if (step < 1) return fail(h, LAMB_EINVAL, "step must be >= 1");
@@ -689,7 +732,13 @@ extern "C" lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void
     lamb_status st = check_async(h);
     if (st != LAMB_OK) return st;
     cudaSetDevice(h->device);
-    st = step_impl(h, grads, step, static_cast<cudaStream_t>(stream), 0, h->plan.n_buckets(), false);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    st = prologue(h, step, s);
+    if (st != LAMB_OK) return st;
+    const bool graph = (h->cfg.flags & LAMB_FLAG_GRAPH) && !grads && !h->pre_b_event &&
+                       !(h->cfg.world_size > 1 && h->cfg.comm_mode == LAMB_COMM_NCCL);
+    if (graph) return graph_step(h, s);
+    st = step_impl(h, grads, step, s, 0, h->plan.n_buckets(), false);
     if (h->t_n < h->t_max) ++h->t_n;
     return st;
 }
@@ -705,8 +754,10 @@ extern "C" lamb_status lamb_step_bucket(lamb_t h, int64_t bucket, int64_t step, 
     cudaSetDevice(h->device);
     const int32_t t_max = h->t_max;
     h->t_max = 0;   // per-bucket calls are not phase-timed
-    st = step_impl(h, nullptr, step, static_cast<cudaStream_t>(stream), bucket, bucket + 1,
-                   (flags & LAMB_BUCKET_DEFER_AG) != 0);
+    st = prologue(h, step, static_cast<cudaStream_t>(stream));
+    if (st == LAMB_OK)
+        st = step_impl(h, nullptr, step, static_cast<cudaStream_t>(stream), bucket, bucket + 1,
+                       (flags & LAMB_BUCKET_DEFER_AG) != 0);
     h->t_max = t_max;
     return st;
 }

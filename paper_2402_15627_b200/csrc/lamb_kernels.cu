@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_a_kernel(const __grid_con
     const float gs = P.clip ? P.clip->gs : P.grad_scale;
     for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
         const Item I = P.items[it];
-        const GroupConst& G = P.groups[I.group];
+        const GroupConst G = P.groups[I.group];
         float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
         float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
         const float4* __restrict__ wp = reinterpret_cast<const float4*>(P.w + I.shard_off);
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_a_pf_kernel(const __grid_
     const float gs = P.clip ? P.clip->gs : P.grad_scale;
     for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
         const Item I = P.items[it];
-        const GroupConst& G = P.groups[I.group];
+        const GroupConst G = P.groups[I.group];
         float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
         float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
         const float4* __restrict__ wp = reinterpret_cast<const float4*>(P.w + I.shard_off);
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_b_kernel(const __grid_con
     if (P.clip && P.clip->skip) return;
     for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
         const Item I = P.items[it];
-        const GroupConst& G = P.groups[I.group];
+        const GroupConst G = P.groups[I.group];
         const float scale = P.scale[I.tensor];
         float4* __restrict__ wp = reinterpret_cast<float4*>(P.w + I.shard_off);
         const float4* __restrict__ mp = reinterpret_cast<const float4*>(P.m + I.shard_off);
@@ -586,6 +586,12 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* _
         dst[i] = __float2bfloat16_rn(src[i]);
 }
 
+// ------------------------------------------------------------ step prologue
+__global__ void prologue_kernel(const __grid_constant__ GroupTable T, int n, GroupConst* dst) {
+    const int i = threadIdx.x;
+    if (i < n) dst[i] = T.g[i];
+}
+
 // ------------------------------------------------------------ host launchers
 // Variant table: unroll U and min-CTAs-per-SM (register cap) per pass.  Defaults from the
 // r01 sweep (profiles/); LAMB_TUNE="ua=U,ma=M,ub=U,mb=M" overrides for tuning runs.
@@ -741,6 +747,11 @@ cudaError_t launch_clip_finalize(const ClipParams& p, cudaStream_t s) {
 
 cudaError_t launch_clip_combine(const ClipParams& p, cudaStream_t s) {
     clip_combine_kernel<<<1, 1, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prologue(const GroupTable& t, int n_groups, GroupConst* dst, cudaStream_t s) {
+    prologue_kernel<<<1, LAMB_MAX_GROUPS, 0, s>>>(t, n_groups, dst);
     return cudaGetLastError();
 }
 

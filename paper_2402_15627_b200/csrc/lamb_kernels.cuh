@@ -81,7 +81,7 @@ struct StepParams {
     const ClipState* clip;    // non-null: pre-step enabled (gs from device, skip flag)
     float* g32_out;           // grad_stats: materialise the fp32 reduced sums here (FUSED + clip)
     __nv_bfloat16* pdst[LAMB_MAX_RANKS];   // param buffers pass B stores into
-    GroupConst groups[LAMB_MAX_GROUPS];
+    const GroupConst* groups;  // device table [n_groups], refreshed each step by the prologue
 };
 
 struct FinalizeParams {
@@ -104,10 +104,17 @@ struct FinalizeParams {
     int32_t n_local_strad;
     const double2* xbuf;            // this rank's exchange buffer
     const ClipState* clip;          // skip flag (pre-step)
-    GroupConst groups[LAMB_MAX_GROUPS];
+    const GroupConst* groups;       // device table [n_groups]
+};
+
+// Per-step constants of every group, written to device memory by one tiny kernel launched on
+// the step's stream before the step (so a captured CUDA graph of the step replays correctly).
+struct GroupTable {
+    GroupConst g[LAMB_MAX_GROUPS];
 };
 
 // Host launchers (lamb_kernels.cu).  `occ_grid` = persistent grid size.
+cudaError_t launch_prologue(const GroupTable& t, int n_groups, GroupConst* dst, cudaStream_t s);
 cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int grid, cudaStream_t s);
 cudaError_t launch_pass_b(const StepParams& p, int ndst, int grid, cudaStream_t s);
 cudaError_t launch_grad_stats(const StepParams& p, int nsrc, bool materialise, int grid, cudaStream_t s);

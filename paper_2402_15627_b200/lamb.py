@@ -29,6 +29,7 @@ LAMB_MAX_RANKS = 8
 LAMB_UNIQUE_ID_BYTES = 128
 LAMB_COMM_NCCL, LAMB_COMM_FUSED = 0, 1
 LAMB_FLAG_TIMING = 1
+LAMB_FLAG_GRAPH = 2
 LAMB_BUCKET_DEFER_AG = 1
 LAMB_BUF_GRAD, LAMB_BUF_PARAM, LAMB_BUF_W, LAMB_BUF_M, LAMB_BUF_V = range(5)
 PHASES = ["barrier_in", "pass_a", "finalize", "exchange", "pass_b", "barrier_out"]
@@ -208,7 +209,7 @@ class Lamb:
     def __init__(self, tensors: Sequence[tuple], groups: Sequence, world_size: int = 1, rank: int = 0,
                  device: int = 0, comm_mode: int = LAMB_COMM_FUSED, bucket_cap: int = 0,
                  grad_scale: float = 0.0, timing: bool = False, unique_id: Optional[bytes] = None,
-                 pg=None):
+                 pg=None, graph: bool = False):
         import torch
         self.torch = torch
         self.device = device
@@ -224,7 +225,7 @@ class Lamb:
             garr[k].eps, garr[k].weight_decay = get("eps"), get("weight_decay")
             garr[k].adapt, garr[k].bias_correction = int(get("adapt")), int(get("bias_correction"))
         cfg = lamb_config(world_size, rank, device, comm_mode, bucket_cap, grad_scale,
-                          LAMB_FLAG_TIMING if timing else 0)
+                          (LAMB_FLAG_TIMING if timing else 0) | (LAMB_FLAG_GRAPH if graph else 0))
         if world_size > 1 and unique_id is None:
             if pg is None:
                 raise ValueError("world_size > 1 needs unique_id or a process group")

@@ -228,6 +228,36 @@ def ckpt_case(world, rank, local, mode):
     dist.barrier()
 
 
+def graph_case(world, rank, local, mode):
+    """FUSED mode under LAMB_FLAG_GRAPH (barriers with device epochs inside the replayed graph)
+    == eager, bitwise."""
+    from paper_2402_15627_b200 import lamb
+    if mode != lamb.LAMB_COMM_FUSED:
+        return
+    rng = np.random.default_rng(107)
+    tensors = W.random_table(rng, 30, max_numel=6000, p_big=0.2, big=40_000)
+    wl = W.Workload("graphd", 75, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    mk = lambda g: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
+                             device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD, graph=g)
+    E, G = mk(False), mk(True)
+    for L in (E, G):
+        L.synth_init(spec, wl.seed)
+    for t in range(1, 5):
+        for L in (E, G):
+            L.synth_grads(spec, wl.seed, rank + 1, t)
+            L.step(t)
+    torch.cuda.synchronize()
+    for k in (2, 3, 4):
+        assert np.array_equal(E.get_state(k).view(np.uint32), G.get_state(k).view(np.uint32)), k
+    assert torch.equal(E.param_buffer().view(torch.int16), G.param_buffer().view(torch.int16))
+    E.close()
+    G.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] CUDA-graph step D={world} == eager (bitwise)", flush=True)
+
+
 def failure_case(world, rank, local, mode):
     """Failure detection: (1) a rank passing a different table makes lamb_create fail on every
     rank; (2) in FUSED mode a rank that skips a step makes the others' barriers time out
@@ -302,6 +332,7 @@ def main():
     clip_case(world, rank, local, mode)
     bucket_case(world, rank, local, mode)
     host_case(world, rank, local, mode)
+    graph_case(world, rank, local, mode)
     os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"
     failure_case(world, rank, local, mode)
     if a.big:

@@ -398,3 +398,31 @@ def test_results_independent_of_grid_and_sm_partition(lamb):
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert np.array_equal(a, b)
+
+
+def test_cuda_graph_step_equals_eager(lamb):
+    """a7: LAMB_FLAG_GRAPH replays one captured graph of the step (constants refreshed by the
+    prologue each step); bit-identical to eager launches, also after a re-capture when the
+    pre-step is switched on."""
+    rng = np.random.default_rng(67)
+    tensors = W.random_table(rng, 30, max_numel=20000, p_big=0.2, big=100_000)
+    wl = W.Workload("graph", 97, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    E = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=50_000)
+    G = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=50_000, graph=True)
+    for L in (E, G):
+        L.synth_init(spec, wl.seed)
+    for t in range(1, 6):
+        if t == 4:
+            for L in (E, G):
+                L.set_grad_clip(0.05)
+        for L in (E, G):
+            L.synth_grads(spec, wl.seed, 1, t)
+            L.step(t)
+    torch.cuda.synchronize()
+    for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V):
+        assert np.array_equal(E.get_state(k).view(np.uint32), G.get_state(k).view(np.uint32))
+    assert torch.equal(E.param_buffer().view(torch.int16), G.param_buffer().view(torch.int16))
+    assert G.step_info()["clip"] < 1.0
+    E.close()
+    G.close()
