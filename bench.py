@@ -294,9 +294,14 @@ def main():
         out["bound"] = "nvlink" if nvl_in and nvl_in / nvl_peak > nbytes / hbm else "hbm"
         return out
 
-    ra = pass_roof("pass_a", bytes_a, t_a, NVLINK_PULL_GBS)
-    rb = pass_roof("pass_b", bytes_b, t_b, NVLINK_PUSH_GBS)
-    dom = ra if t_a >= t_b else rb
+    if args.graph:
+        # no per-kernel events inside a replayed graph: the whole step against its bytes
+        ra = rb = dom = pass_roof("step(graph)", bytes_a + bytes_b, ms, NVLINK_PULL_GBS)
+        nvl_in = 0
+    else:
+        ra = pass_roof("pass_a", bytes_a, t_a, NVLINK_PULL_GBS)
+        rb = pass_roof("pass_b", bytes_b, t_b, NVLINK_PUSH_GBS)
+        dom = ra if t_a >= t_b else rb
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
