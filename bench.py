@@ -295,9 +295,9 @@ def main():
         return out
 
     if args.graph:
-        # no per-kernel events inside a replayed graph: the whole step against its bytes
-        ra = rb = dom = pass_roof("step(graph)", bytes_a + bytes_b, ms, NVLINK_PULL_GBS)
+        # no per-kernel events inside a replayed graph: the whole step against its HBM bytes
         nvl_in = 0
+        ra = rb = dom = pass_roof("step(graph)", bytes_a + bytes_b, ms, NVLINK_PULL_GBS)
     else:
         ra = pass_roof("pass_a", bytes_a, t_a, NVLINK_PULL_GBS)
         rb = pass_roof("pass_b", bytes_b, t_b, NVLINK_PUSH_GBS)
