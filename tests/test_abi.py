@@ -49,6 +49,8 @@ def test_errors_without_gpu_are_reported(L):
     assert st == L.LAMB_EINVAL and b"beta2" in L.lamb_last_error(None)
     with pytest.raises(L.LambError):
         L.host_plan([5, 0], 1, 0)
+    h0 = ctypes.c_void_p()
+    assert L.lamb_plan_create(t, 0, 1, 0, 0, ctypes.byref(h0)) == L.LAMB_EINVAL   # empty table
     with pytest.raises(L.LambError):
         L.host_plan([5], 9, 0)
     with pytest.raises(L.LambError):

@@ -426,3 +426,24 @@ def test_cuda_graph_step_equals_eager(lamb):
     assert G.step_info()["clip"] < 1.0
     E.close()
     G.close()
+
+
+def test_max_size_tensor_beyond_int32(lamb):
+    """Maximum-size edge case: one tensor of 2^31 + 3 elements (flat, shard and in-tensor
+    offsets beyond int32; 537k work items in one segment) next to a 1-element tensor, one
+    step, every element against the oracle."""
+    big = 2 ** 31 + 3
+    tensors = [W.TensorSpec("huge", big, W.DECAY, W.INIT_UNIFORM, W.GEXP_MATRIX),
+               W.TensorSpec("one", 1, W.NO_DECAY, W.INIT_ONE, W.GEXP_VECTOR)]
+    wl = W.Workload("max", 98, tensors, W.default_groups(lr=2.0 ** -7))
+    L = run_gpu(wl, steps=1, cap=0)
+    assert L.plan.flat_size > 2 ** 31
+    orc = oracle.OracleRun(wl)
+    orc.step(1)
+    compare_state(L, orc, 1, ids=[0, 1], check_params=False)
+    p = L.param_buffer()
+    for lo in (0, 2 ** 31 - 8, big - 8):          # params around the int32 boundary and the end
+        got = p[lo:lo + 8].view(torch.int16).cpu().numpy().view(np.uint16)
+        w = L.state_buffer(lamb.LAMB_BUF_W)[lo:lo + 8].cpu().numpy().astype(np.float64)
+        assert np.array_equal(got, oracle.bf16_rne_bits(w))
+    L.close()
