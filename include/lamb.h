@@ -188,6 +188,10 @@ lamb_status lamb_query_plan(lamb_t h, lamb_plan_view* out);
 #define LAMB_BUF_W 2       /* fp32 [shard_size] master weights, shard-local order */
 #define LAMB_BUF_M 3       /* fp32 [shard_size] first moment (stored uncorrected, Z5) */
 #define LAMB_BUF_V 4       /* fp32 [shard_size] second moment */
+#define LAMB_BUF_GSUM 5    /* fp32 [shard_size] reduced gradient sum_j G_j of the last step
+                              (before grad_scale), shard order; exists only where the path
+                              materialises it: NCCL mode, or FUSED with the pre-step enabled
+                              (else LAMB_ESTATE) — for exactness checks (pin H10) */
 /* Device pointer + element count of a library buffer; valid until lamb_destroy. */
 lamb_status lamb_buffer(lamb_t h, int32_t which, void** dev_ptr, int64_t* n_elems);
 

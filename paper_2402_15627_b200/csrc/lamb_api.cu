@@ -843,6 +843,11 @@ extern "C" lamb_status lamb_buffer(lamb_t h, int32_t which, void** dev_ptr, int6
         case LAMB_BUF_W: *dev_ptr = h->w; *n = h->plan.shard_size; return LAMB_OK;
         case LAMB_BUF_M: *dev_ptr = h->m; *n = h->plan.shard_size; return LAMB_OK;
         case LAMB_BUF_V: *dev_ptr = h->v; *n = h->plan.shard_size; return LAMB_OK;
+        case LAMB_BUF_GSUM:
+            if (!h->g32) return fail(h, LAMB_ESTATE, "no materialised reduced gradient on this path");
+            *dev_ptr = h->g32;
+            *n = h->plan.shard_size;
+            return LAMB_OK;
     }
     return fail(h, LAMB_EINVAL, "unknown buffer");
 }

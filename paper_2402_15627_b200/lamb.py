@@ -31,7 +31,7 @@ LAMB_COMM_NCCL, LAMB_COMM_FUSED = 0, 1
 LAMB_FLAG_TIMING = 1
 LAMB_FLAG_GRAPH = 2
 LAMB_BUCKET_DEFER_AG = 1
-LAMB_BUF_GRAD, LAMB_BUF_PARAM, LAMB_BUF_W, LAMB_BUF_M, LAMB_BUF_V = range(5)
+LAMB_BUF_GRAD, LAMB_BUF_PARAM, LAMB_BUF_W, LAMB_BUF_M, LAMB_BUF_V, LAMB_BUF_GSUM = range(6)
 PHASES = ["barrier_in", "pass_a", "finalize", "exchange", "pass_b", "barrier_out"]
 LAMB_N_PHASES = len(PHASES)
 

@@ -258,6 +258,34 @@ def graph_case(world, rank, local, mode):
         print(f"[ok] CUDA-graph step D={world} == eager (bitwise)", flush=True)
 
 
+def h10_case(world, rank, local, mode):
+    """Pin H10 on the GPU: the fp32 reduced gradient (NCCL reduce-scatter of the upcast grads,
+    or the fused peer-load sum) equals the exact D-rank sum bit-for-bit (the generator's
+    values make the fp32 sum exact in any order)."""
+    from paper_2402_15627_b200 import lamb
+    rng = np.random.default_rng(109)
+    tensors = W.random_table(rng, 25, max_numel=6000, p_big=0.2, big=40_000)
+    wl = W.Workload("h10", 76, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    L = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank, device=local,
+                  comm_mode=mode, bucket_cap=10_000, pg=dist.group.WORLD)
+    L.synth_init(spec, wl.seed)
+    if mode == lamb.LAMB_COMM_FUSED:
+        L.set_grad_clip(1e30)            # the fused path materialises the sum in its pre-step
+    L.synth_grads(spec, wl.seed, rank + 1, 1)
+    L.step(1)
+    torch.cuda.synchronize()
+    gsum = L.state_buffer(lamb.LAMB_BUF_GSUM).cpu().numpy().astype(np.float64)
+    for (i, soff, toff, ln) in L.plan.segments.tolist():
+        ts = tensors[i]
+        exact = sum(oracle.gen_grads(wl.seed, j + 1, i, 1, ts.gexp, ts.numel) for j in range(world))
+        assert np.array_equal(gsum[soff:soff + ln], exact[toff:toff + ln]), i
+    L.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] H10 exact fp32 reduce-scatter D={world} mode={mode}", flush=True)
+
+
 def failure_case(world, rank, local, mode):
     """Failure detection: (1) a rank passing a different table makes lamb_create fail on every
     rank; (2) in FUSED mode a rank that skips a step makes the others' barriers time out
@@ -333,6 +361,7 @@ def main():
     bucket_case(world, rank, local, mode)
     host_case(world, rank, local, mode)
     graph_case(world, rank, local, mode)
+    h10_case(world, rank, local, mode)
     os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"
     failure_case(world, rank, local, mode)
     if a.big:
