@@ -72,6 +72,7 @@ struct lamb_ctx {
     cudaEvent_t pre_b_event = nullptr;   // step_impl waits on it before pass B (lamb_step_host)
     int grid_a = 0, grid_b = 0;
     int max_ctas = 0;   // SM budget of the streaming passes (0 = one full wave)
+    bool diag_local_grads = false;   // LAMB_DIAG_LOCAL_GRADS: timing diagnostic, wrong results
     lamb::GroupConst* d_groups = nullptr;   // per-step group constants (prologue kernel)
     // LAMB_FLAG_GRAPH
     cudaGraphExec_t graph_exec = nullptr;

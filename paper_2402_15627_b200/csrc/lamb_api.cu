@@ -340,6 +340,7 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
 
     auto* h = new lamb_ctx();
     h->cfg = *cfg;
+    h->diag_local_grads = getenv("LAMB_DIAG_LOCAL_GRADS") != nullptr;
     {
         // failure detection: bound on every cross-GPU wait (a missing peer must not hang the GPU)
         const char* e = getenv("LAMB_BARRIER_TIMEOUT_MS");
@@ -558,6 +559,8 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         mark(h, 1, s);
         for (int j = 0; j < D; ++j)
             sp.gsrc[j] = fused ? h->peer_grad[j] : (grads ? (const __nv_bfloat16*)grads : h->grad);
+        if (fused && h->diag_local_grads)   // timing diagnostic only (wrong sums): no NVLink loads
+            for (int j = 0; j < D; ++j) sp.gsrc[j] = h->grad;
         if (pre) {
             // pre-step: global ||g||^2 (FUSED: the reduce-scatter happens here, into g32)
             sp.g32_out = h->g32;
