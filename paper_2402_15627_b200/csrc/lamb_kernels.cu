@@ -263,6 +263,96 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_a_pf_kernel(const __grid_
     }
 }
 
+// Pass A with a shared-memory ring for the gradient words (FUSED, NS >= 2): every lane
+// streams its own future gradient chunks (NS x 8 B per chunk, mostly remote) with cp.async,
+// P-1 U-blocks ahead of use, so NVLink latency is covered without holding registers.  A lane
+// only ever reads back what it copied itself (wait_group makes its own copies visible), so no
+// warp synchronisation is needed.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NS, int U, int PD>
+__global__ void __launch_bounds__(kThreads, 2) pass_a_ring_kernel(const __grid_constant__ StepParams P_) {
+    const StepParams& P = P_;
+    extern __shared__ __align__(16) uint2 ring_all[];   // [warps][P][U][NS][32]
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    uint2* ring = ring_all + (size_t)wib * PD * U * NS * 32;
+    const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
+    if (P.clip && P.clip->skip) return;
+    const float gs = P.clip ? P.clip->gs : P.grad_scale;
+    auto slot = [&](int stage, int k, int j) -> uint2* { return ring + (((stage * U + k) * NS + j) * 32 + lane); };
+    for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
+        const Item I = P.items[it];
+        const GroupConst G = P.groups[I.group];
+        float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
+        float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
+        const float4* __restrict__ wp = reinterpret_cast<const float4*>(P.w + I.shard_off);
+        const int n = I.n_chunk;
+        const int nb = n / (32 * U);   // full U-blocks (same for every lane)
+        auto issue = [&](int b) {
+            if (b < nb) {
+                const int stage = b % PD;
+#pragma unroll
+                for (int k = 0; k < U; ++k)
+#pragma unroll
+                    for (int j = 0; j < NS; ++j)
+                        cp_async8(slot(stage, k, j),
+                                  reinterpret_cast<const uint2*>(P.gsrc[j] + I.flat_off) + 32 * U * b + 32 * k + lane);
+            }
+            cp_async_commit();   // always commit: keeps the group count uniform
+        };
+#pragma unroll
+        for (int b = 0; b < PD - 1; ++b) issue(b);
+        double dw = 0.0, du = 0.0;
+        for (int b = 0; b < nb; ++b) {
+            issue(b + PD - 1);
+            const int c = 32 * U * b + lane;
+            float4 m[U], v[U], w[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                m[k] = __ldcs(mp + c + 32 * k);
+                v[k] = __ldcs(vp + c + 32 * k);
+                w[k] = __ldcs(wp + c + 32 * k);
+            }
+            cp_async_wait<PD - 1>();   // this lane's copies of block b have landed
+            const int stage = b % PD;
+            float sw = 0.f, su = 0.f;
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                uint2 raw[NS];
+#pragma unroll
+                for (int j = 0; j < NS; ++j) raw[j] = *slot(stage, k, j);
+                chunk_a(sum_raw<NS>(raw), m[k], v[k], w[k], gs, G, sw, su);
+                __stcs(mp + c + 32 * k, m[k]);
+                __stcs(vp + c + 32 * k, v[k]);
+            }
+            dw += (double)sw;
+            du += (double)su;
+        }
+        cp_async_wait<0>();
+        for (int c = 32 * U * nb + lane; c < n; c += 32) {
+            float4 g = load_grad<NS>(P, I, 4 * (int64_t)c), m = __ldcs(mp + c), v = __ldcs(vp + c);
+            const float4 w = __ldcs(wp + c);
+            float sw = 0.f, su = 0.f;
+            chunk_a(g, m, v, w, gs, G, sw, su);
+            __stcs(mp + c, m);
+            __stcs(vp + c, v);
+            dw += (double)sw;
+            du += (double)su;
+        }
+        dw = warp_sum(dw);
+        du = warp_sum(du);
+        if (lane == 0) P.partials[it] = make_double2(dw, du);
+    }
+}
+
 // ------------------------------------------------------------ pass B
 __device__ __forceinline__ uint2 chunk_b(const float4 m, const float4 v, float4& w, float scale,
                                          const GroupConst& G) {
@@ -598,11 +688,13 @@ __global__ void prologue_kernel(const __grid_constant__ GroupTable T, int n, Gro
 struct Tune {
     int ua = 4, ma = 2, ub = 4, mb = 2;
     int pf = 1, upf = 4;   // FUSED (NS >= 2): prefetching pass A (U = 4 for NS = 2, else 2; r01 sweep)
+    int ring = 0;          // FUSED (NS >= 2): cp.async smem ring of this depth (0 = off)
 };
 static Tune g_tune = [] {
     Tune t;
     if (const char* e = getenv("LAMB_TUNE")) {
-        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d", &t.ua, &t.ma, &t.ub, &t.mb, &t.pf, &t.upf);
+        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d,ring=%d", &t.ua, &t.ma, &t.ub, &t.mb, &t.pf, &t.upf,
+               &t.ring);
     }
     return t;
 }();
@@ -618,9 +710,26 @@ static cudaError_t pass_a_pf(const StepParams& p, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int NS, int U, int PD>
+static cudaError_t pass_a_ring(const StepParams& p, int grid, cudaStream_t s) {
+    const size_t smem = (size_t)(kThreads / 32) * PD * U * NS * 32 * sizeof(uint2);
+    static bool attr = [&] {
+        cudaFuncSetAttribute(pass_a_ring_kernel<NS, U, PD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+    }();
+    (void)attr;
+    pass_a_ring_kernel<NS, U, PD><<<grid, kThreads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <int NS>
 static cudaError_t pass_a_ns(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
+    if constexpr (NS >= 2 && NS <= 4) {
+        if (t.ring == 3) return pass_a_ring<NS, 4, 3>(p, grid, s);
+        if (t.ring == 4) return pass_a_ring<NS, 4, 4>(p, grid, s);
+        if (t.ring == 6) return pass_a_ring<NS, 2, 6>(p, grid, s);
+    }
     if constexpr (NS >= 2) {
         if (t.pf) {
             if constexpr (NS == 2) {   // U = 4 fits the register budget only for two sources
