@@ -1,0 +1,96 @@
+"""`LambOptimizer`: use the sharded LAMB step from a PyTorch training loop.
+
+Marshalling only — the step is `lamb_step` of liblamb.so.  The model's parameters are re-pointed
+to views of the library's flat bf16 PARAM buffer, and their `.grad` to views of the flat bf16
+GRAD buffer, so autograd accumulates straight into the buffer the fused reduce-scatter reads
+and the updated (all-gathered) bf16 parameters are what the next forward uses — no copies.
+The fp32 master weights and Adam moments live in the library's shards (ZeRO-2, §2
+P:689-701); LAMB per PAPER.md §3.1 P:288-293 (update rule and readings: DESIGN.md §3).
+
+    opt = LambOptimizer(model.parameters(), lr=1e-3, weight_decay=0.01, pg=dist.group.WORLD)
+    for batch in data:
+        opt.zero_grad()
+        loss(model(batch)).backward()
+        opt.step()
+
+Parameter groups follow torch.optim conventions ([{"params": [...], "lr": ..., ...}, ...]).
+Parameters must be bf16 CUDA tensors on this rank's device.
+"""
+from __future__ import annotations
+
+from typing import Iterable, List, Optional
+
+import torch
+
+from . import lamb
+
+
+class LambOptimizer:
+    def __init__(self, params: Iterable, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-6,
+                 weight_decay: float = 0.0, adapt: bool = True, bias_correction: bool = True,
+                 world_size: int = 1, rank: int = 0, pg=None, comm_mode: int = lamb.LAMB_COMM_FUSED,
+                 bucket_cap: int = 0, max_grad_norm: float = 0.0, graph: bool = False):
+        params = list(params)
+        if params and not isinstance(params[0], dict):
+            params = [{"params": params}]
+        defaults = dict(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay,
+                        adapt=int(adapt), bias_correction=int(bias_correction))
+        self.groups: List[dict] = []
+        self.params: List[torch.nn.Parameter] = []
+        table = []
+        for gi, g in enumerate(params):
+            hp = dict(defaults)
+            for k_in, k_out in (("lr", "lr"), ("eps", "eps"), ("weight_decay", "weight_decay")):
+                if k_in in g:
+                    hp[k_out] = g[k_in]
+            if "betas" in g:
+                hp["beta1"], hp["beta2"] = g["betas"]
+            self.groups.append(hp)
+            for p in g["params"]:
+                if p.dtype != torch.bfloat16 or not p.is_cuda:
+                    raise TypeError("LambOptimizer manages bf16 CUDA parameters")
+                self.params.append(p)
+                table.append((p.numel(), gi))
+        if not self.params:
+            raise ValueError("no parameters")
+        self.device = self.params[0].device.index or 0
+        self.L = lamb.Lamb(table, self.groups, world_size=world_size, rank=rank, device=self.device,
+                           comm_mode=comm_mode, bucket_cap=bucket_cap, pg=pg, graph=graph)
+        # fp32 master = the current bf16 values (exact), then the params become buffer views
+        flat = torch.zeros(self.L.plan.flat_size, dtype=torch.float32, device=f"cuda:{self.device}")
+        for p, off in zip(self.params, self.L.plan.tensor_off.tolist()):
+            flat[off:off + p.numel()] = p.detach().reshape(-1).float()
+        self.L.set_master(flat)
+        del flat
+        pv, gv = self.L.param_views(), self.L.grad_views()
+        for p, v, g in zip(self.params, pv, gv):
+            p.data = v.view(p.shape)
+            p.grad = g.view(p.shape)
+        if max_grad_norm > 0:
+            self.L.set_grad_clip(max_grad_norm)
+        self.t = 0
+
+    @torch.no_grad()
+    def zero_grad(self, set_to_none: bool = False) -> None:
+        # the grad views ARE the library's flat buffer (padding stays zero)
+        self.L.grad_buffer().zero_()
+
+    @torch.no_grad()
+    def step(self, closure=None) -> None:
+        for p, g in zip(self.params, self.L.grad_views()):   # autograd may have replaced .grad
+            if p.grad is not None and p.grad.data_ptr() != g.data_ptr():
+                g.view(p.shape).copy_(p.grad)
+                p.grad = g.view(p.shape)
+        self.t += 1
+        self.L.step(self.t)
+
+    def set_lr(self, lr: float, group: Optional[int] = None) -> None:
+        for gi in ([group] if group is not None else range(len(self.groups))):
+            self.L.set_lr(gi, lr)
+
+    def state_dict_path(self, path: str) -> None:
+        """Two-stage checkpoint of the sharded state (lamb_checkpoint_save)."""
+        self.L.checkpoint_save(path, self.t)
+
+    def load_path(self, path: str) -> None:
+        self.t = self.L.checkpoint_load(path)

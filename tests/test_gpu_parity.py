@@ -447,3 +447,50 @@ def test_max_size_tensor_beyond_int32(lamb):
         w = L.state_buffer(lamb.LAMB_BUF_W)[lo:lo + 8].cpu().numpy().astype(np.float64)
         assert np.array_equal(got, oracle.bf16_rne_bits(w))
     L.close()
+
+
+def test_torch_optimizer_binding_end_to_end(lamb):
+    """LambOptimizer drives lamb_step from a real PyTorch loop (bf16 MLP): params are views of
+    the library's param buffer, autograd accumulates into its grad buffer; three iterations
+    against the oracle fed the same captured gradients (exact bf16 values, D = 1)."""
+    from paper_2402_15627_b200.torch_optim import LambOptimizer
+    torch.manual_seed(0)
+    model = torch.nn.Sequential(torch.nn.Linear(96, 200), torch.nn.GELU(), torch.nn.Linear(200, 33)).cuda().bfloat16()
+    weights = [p for n, p in model.named_parameters() if p.dim() > 1]
+    biases = [p for n, p in model.named_parameters() if p.dim() == 1]
+    groups = [{"params": weights, "weight_decay": 0.01}, {"params": biases, "weight_decay": 0.0}]
+    ordered = weights + biases
+    w0 = [p.detach().double().cpu().numpy().reshape(-1).copy() for p in ordered]
+    opt = LambOptimizer(groups, lr=2.0 ** -7, betas=(0.9, 0.999), eps=1e-6)
+    x = torch.randn(64, 96, device="cuda", dtype=torch.bfloat16)
+    grads = []
+    for _ in range(3):
+        opt.zero_grad()
+        model(x).float().pow(2).mean().backward()
+        grads.append([p.grad.detach().double().cpu().numpy().reshape(-1).copy() for p in ordered])
+        opt.step()
+    torch.cuda.synchronize()
+    # the oracle, tensor by tensor, on the captured gradients
+    class Grp:
+        def __init__(self, wd):
+            self.lr, self.beta1, self.beta2, self.eps = 2.0 ** -7, 0.9, 0.999, 1e-6
+            self.weight_decay, self.adapt, self.bias_correction = wd, 1, 1
+    state = []
+    for k, wk in enumerate(w0):
+        grp = Grp(0.01 if k < len(weights) else 0.0)
+        w, m, v = wk.copy(), np.zeros_like(wk), np.zeros_like(wk)
+        for t in range(3):
+            oracle.lamb_tensor_step(w, m, v, grads[t][k], grp, t + 1)
+        state.append((w, m, v))
+    Wg, Mg, Vg = (opt.L.get_state(b) for b in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V))
+    for (i, soff, toff, ln) in opt.L.plan.segments.tolist():
+        w, m, v = state[i]
+        for got, ref in ((Wg, w), (Mg, m), (Vg, v)):
+            g = got[soff:soff + ln].astype(np.float64)
+            r = ref[toff:toff + ln]
+            atol = 1e-6 if ref is w else 1e-6 * np.max(np.abs(ref))
+            assert np.all(np.abs(g - r) <= atol + 1e-4 * np.abs(r)), i
+        # the model's parameter IS bf16_rne of the master
+        pb = ordered[i].detach().reshape(-1)[toff:toff + ln].view(torch.int16).cpu().numpy().view(np.uint16)
+        assert np.array_equal(pb, oracle.bf16_rne_bits(Wg[soff:soff + ln].astype(np.float64)))
+    opt.L.close()
