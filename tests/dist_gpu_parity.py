@@ -286,6 +286,59 @@ def h10_case(world, rank, local, mode):
         print(f"[ok] H10 exact fp32 reduce-scatter D={world} mode={mode}", flush=True)
 
 
+def torch_case(world, rank, local, mode):
+    """Data-parallel training loop through LambOptimizer: identical bf16 model replicas, a
+    different batch per rank; the step must equal the oracle's LAMB on the mean of the ranks'
+    (captured) gradients (ZeRO-2 semantics)."""
+    from paper_2402_15627_b200 import lamb
+    from paper_2402_15627_b200.torch_optim import LambOptimizer
+    torch.manual_seed(0)
+    model = torch.nn.Sequential(torch.nn.Linear(64, 300), torch.nn.GELU(), torch.nn.Linear(300, 17)).cuda().bfloat16()
+    ordered = [p for _, p in model.named_parameters()]
+    w0 = [p.detach().double().cpu().numpy().reshape(-1).copy() for p in ordered]
+    opt = LambOptimizer(model.parameters(), lr=2.0 ** -7, weight_decay=0.01, world_size=world, rank=rank,
+                        pg=dist.group.WORLD, comm_mode=mode, bucket_cap=5000)
+    g_all = []
+    torch.manual_seed(1 + rank)          # different data per rank
+    for _ in range(2):
+        x = torch.randn(32, 64, device="cuda", dtype=torch.bfloat16)
+        opt.zero_grad()
+        model(x).float().pow(2).mean().backward()
+        mine = torch.cat([p.grad.detach().reshape(-1).float() for p in ordered])
+        gathered = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(gathered, mine)
+        g_all.append(torch.stack(gathered).double().cpu().numpy())
+        opt.step()
+    torch.cuda.synchronize()
+
+    class Grp:
+        lr, beta1, beta2, eps, weight_decay, adapt, bias_correction = 2.0 ** -7, 0.9, 0.999, 1e-6, 0.01, 1, 1
+    offs = np.cumsum([0] + [w.size for w in w0])
+    state = []
+    for k, wk in enumerate(w0):
+        w, m, v = wk.copy(), np.zeros_like(wk), np.zeros_like(wk)
+        for t in range(2):
+            g = oracle.reduce([g_all[t][j][offs[k]:offs[k + 1]].copy() for j in range(world)], 1.0 / world)
+            oracle.lamb_tensor_step(w, m, v, g, Grp, t + 1)
+        state.append((w, m))
+    Wg, Mg = opt.L.get_state(lamb.LAMB_BUF_W), opt.L.get_state(lamb.LAMB_BUF_M)
+    for (i, soff, toff, ln) in opt.L.plan.segments.tolist():
+        w, m = state[i]
+        for got, ref, atol in ((Wg, w, 1e-6), (Mg, m, 1e-6 * np.max(np.abs(m)))):
+            gg = got[soff:soff + ln].astype(np.float64)
+            r = ref[toff:toff + ln]
+            assert np.all(np.abs(gg - r) <= atol + 1e-4 * np.abs(r)), i
+    # every rank's model now holds the same (all-gathered) parameters
+    flat = torch.cat([p.detach().reshape(-1) for p in ordered]).view(torch.int16).long()
+    hs = [torch.empty_like(flat) for _ in range(world)]
+    dist.all_gather(hs, flat)
+    assert all(torch.equal(h, hs[0]) for h in hs)
+    opt.L.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] LambOptimizer DP loop D={world} mode={mode} == oracle on mean grads", flush=True)
+
+
 def failure_case(world, rank, local, mode):
     """Failure detection: (1) a rank passing a different table makes lamb_create fail on every
     rank; (2) in FUSED mode a rank that skips a step makes the others' barriers time out
@@ -362,6 +415,7 @@ def main():
     host_case(world, rank, local, mode)
     graph_case(world, rank, local, mode)
     h10_case(world, rank, local, mode)
+    torch_case(world, rank, local, mode)
     os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"
     failure_case(world, rank, local, mode)
     if a.big:
