@@ -397,6 +397,9 @@ def main():
         wl = W.gpt_13b()
         ids = [1, 2, 3, 4, 6, 7, 8, 10, 12, 13, 14, 481, 482]
         run_case("gpt13b(full size)", wl, world, rank, local, mode, 1, ids=ids, check_all_params=False)
+        wl = W.slice_175b(12)   # BASELINE configs[3]: every LN/bias vector + one 603M-element fc1
+        ids = [i for i, t in enumerate(wl.tensors) if t.numel <= 4 * 12288] + [8]
+        run_case("175b_slice(full size)", wl, world, rank, local, mode, 1, ids=ids, check_all_params=False)
         dist.barrier()
         dist.destroy_process_group()
         return

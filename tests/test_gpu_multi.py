@@ -46,7 +46,8 @@ def test_parity_8gpu_fused():
 
 
 @pytest.mark.skipif(NGPU < 4, reason="needs >= 4 GPUs")
-def test_full_size_530b_stress_and_13b_4gpu():
-    """BASELINE configs[2] and [4] at full size on 4 GPUs (141 GB/GPU for 530B+stress): every
-    stress / LayerNorm tensor of the 530B slice and sampled 13B tensors against the oracle."""
+def test_full_size_530b_stress_13b_175b_4gpu():
+    """BASELINE configs[2], [3] and [4] at full size on 4 GPUs (141 / 90 / 152 GB per GPU):
+    every stress / LayerNorm tensor of the 530B slice, sampled 13B tensors, and every vector
+    plus one 603M-element matrix of the 175B slice against the oracle."""
     _torchrun(4, "--mode", "fused", "--full", timeout=1800)
