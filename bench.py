@@ -332,7 +332,7 @@ def main():
 
     line = {"metric": METRIC, "value": wl.n_params / (ms / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": K, "warmup": Wm, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (bf16 grads/params)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Philox4x32-10 grads/weights, DESIGN.md §4)",
             "config": {"workload": wl.name, "n_params": wl.n_params, "n_tensors": len(wl.tensors),
                        "flat_size": L.plan.flat_size, "world_size": world,
@@ -340,6 +340,7 @@ def main():
                        "prestep_clip": args.clip if args.clip > 0 else None,
                        "cuda_graph": bool(args.graph),
                        "l2": "inputs larger than L2 (fp32 state of the shard >> 126 MB)",
+                       "io_dtype": "bf16 grads in / bf16 params out, fp32 master and moments",
                        "parallelism": f"zero2-dp{world}"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "host_enqueue_us_per_step": host_us,
