@@ -409,6 +409,14 @@ def main():
     tensors = W.random_table(rng, 60, max_numel=4000, p_big=0.15, big=50_000)
     run_case("ragged", W.Workload("ragged", 50, tensors, W.default_groups(lr=2.0 ** -7)), world, rank,
              local, mode, 3, cap=8192)
+    rng = np.random.default_rng(323)
+    tensors = [W.TensorSpec(f"x{k}", int(rng.integers(1, 30000)), k % 4, W.INIT_UNIFORM, W.GEXP_MATRIX)
+               for k in range(16)]
+    groups = [W.GroupSpec(lr=2.0 ** -7, weight_decay=0.01, adapt=0),
+              W.GroupSpec(lr=2.0 ** -7, weight_decay=0.0, bias_correction=0),
+              W.GroupSpec(lr=0.0, weight_decay=0.01),
+              W.GroupSpec(lr=2.0 ** -8, weight_decay=0.5, beta1=0.8, beta2=0.99, eps=1e-8)]
+    run_case("groups", W.Workload("groups", 52, tensors, groups), world, rank, local, mode, 3, cap=20_000)
     stress = W.stress_tensors(0, 3000)
     run_case("stress", W.Workload("stress", 51, stress, W.default_groups()), world, rank, local, mode, 2,
              cap=100_000)
