@@ -93,6 +93,51 @@ __global__ void rs_uc_bf16(Peers P, int D, float* out, size_t off, size_t bytes)
     }
 }
 
+// Pipelined pair: half the blocks reduce-scatter region A while the other half all-gather
+// region B (RS of bucket b+1 || AG of bucket b).  mc: multimem ld_reduce + multimem.st;
+// uc: peer loads + peer stores (the fused passes' patterns).
+__global__ void pipe_mc(char* mc, const char* mine, float* out, size_t offA, size_t offB, size_t bytes) {
+    const unsigned half = gridDim.x / 2;
+    const bool rs = blockIdx.x < half;
+    const size_t b0 = (size_t)(rs ? blockIdx.x : blockIdx.x - half);
+    for (size_t i = (b0 * blockDim.x + threadIdx.x) * 16; i < bytes; i += (size_t)half * blockDim.x * 16) {
+        if (rs) {
+            uint32_t a, b, c, d;
+            asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(mc + offA + i) : "memory");
+            *reinterpret_cast<uint4*>(reinterpret_cast<char*>(out) + i) = make_uint4(a, b, c, d);
+        } else {
+            const uint4 v = *reinterpret_cast<const uint4*>(mine + offB + i);
+            asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + offB + i),
+                         "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+        }
+    }
+}
+
+__global__ void pipe_uc(Peers P, int D, int me, float* out, size_t offA, size_t offB, size_t bytes) {
+    const unsigned half = gridDim.x / 2;
+    const bool rs = blockIdx.x < half;
+    const size_t b0 = (size_t)(rs ? blockIdx.x : blockIdx.x - half);
+    for (size_t i = (b0 * blockDim.x + threadIdx.x) * 16; i < bytes; i += (size_t)half * blockDim.x * 16) {
+        if (rs) {
+            float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int j = 0; j < D; ++j) {
+                const uint4 v = __ldcs(reinterpret_cast<const uint4*>(P.p[j] + offA + i));
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                for (int k = 0; k < 4; ++k) {
+                    s[2 * k] += __uint_as_float(w[k] << 16);
+                    s[2 * k + 1] += __uint_as_float(w[k] & 0xffff0000u);
+                }
+            }
+            for (int k = 0; k < 8; ++k) out[i / 2 + k] = s[k];
+        } else {
+            const uint4 v = *reinterpret_cast<const uint4*>(P.p[me] + offB + i);
+            for (int j = 0; j < D; ++j)
+                if (j != me) *reinterpret_cast<uint4*>(P.p[j] + offB + i) = v;
+        }
+    }
+}
+
 int main(int argc, char** argv) {
     const int D = argc > 1 ? atoi(argv[1]) : 2;
     const size_t mib = argc > 2 ? (size_t)atoll(argv[2]) : 1024;
@@ -197,7 +242,17 @@ int main(int argc, char** argv) {
     float t_rs_mcb = timeit([&](int g) { rs_mc_bf16<<<grid, blk>>>(mcp, out[g], g * slice, slice); });
     float t_rs_mcf = timeit([&](int g) { rs_mc_f32<<<grid, blk>>>(mcp + bytes, out[g], 2 * g * slice, 2 * slice); });
     float t_rs_uc = timeit([&](int g) { rs_uc_bf16<<<grid, blk>>>(P, D, out[g], g * slice, slice); });
+    // pipelined RS(A) || AG(B): regions A = [0, bytes/2), B = [bytes/2, bytes) of the bf16 buffer
+    const size_t hs = bytes / 2 / D;   // per-GPU slice of each region
+    float t_pipe_mc = timeit([&](int g) { pipe_mc<<<grid, blk>>>(mcp, uva[g], out[g], g * hs, bytes / 2 + g * hs, hs); });
+    float t_pipe_uc = timeit([&](int g) { pipe_uc<<<grid, blk>>>(P, D, g, out[g], g * hs, bytes / 2 + g * hs, hs); });
+    float t_seq_uc = timeit([&](int g) {
+        rs_uc_bf16<<<grid, blk>>>(P, D, out[g], g * hs, hs);
+        ag_uc<<<grid, blk>>>(P, D, g, bytes / 2 + g * hs, hs);
+    });
     CK(cudaGetLastError());
+    printf("{\"D\": %d, \"pipelined_half_buffers\": 1, \"rs_then_ag_uc_ms\": %.3f, \"rs_par_ag_uc_ms\": %.3f, "
+           "\"rs_par_ag_mc_ms\": %.3f}\n", D, t_seq_uc, t_pipe_uc, t_pipe_mc);
     auto gbs = [&](double b, float ms) { return b / (ms * 1e-3) / 1e9; };
     printf("{\"D\": %d, \"MiB\": %zu, \"multicast_supported\": 1, \"slice_MiB\": %.1f, "
            "\"ag_mc_ms\": %.3f, \"ag_uc_ms\": %.3f, \"rs_mc_bf16_ms\": %.3f, \"rs_mc_f32_ms\": %.3f, \"rs_uc_bf16_ms\": %.3f, "
