@@ -4,7 +4,7 @@
 //          the ranks' bf16 grad buffers read over NVLink, fp32 sum in fixed order j=0..D-1]
 //          m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2       [Adam moments, You et al. Alg. 2]
 //          u = (m c1) / (sqrt(v c2) + eps) + wd w            [bias correction Z5, eps Z4, Z7]
-//          per item: sum w^2, sum u^2 in fp64                 [segmented norms, row a3]
+//          per item: sum w^2, sum u^2 (fp32 per 16-element block, then fp64) [row a3]
 // Finalize (a3+a4): per segment fixed-order sum of item partials; straddlers exchanged over
 //          NVLink and summed in rank order; ratio = ||w||/||u|| (1 on a zero norm, Z9).
 // Pass B  (a5+a6): recompute u bit-identically, w -= (lr ratio) u, p = bf16_rne(w) stored to
@@ -12,8 +12,9 @@
 // PAPER.md cites: LAMB §3.1; ZeRO-2 RS/AG §2, §3.2 P:312-328.
 //
 // All three are HBM/NVLink streaming kernels (~1 flop/B): no tensor cores.  Design for B200:
-// 128-bit coalesced loads with L1::no_allocate, several independent chunks per lane in
-// flight, a persistent grid of (148 x resident CTAs) warps walking the item table.
+// 128-bit coalesced streaming loads/stores (ld/st.global.cs, evict-first), several independent
+// chunks per lane in flight, a persistent grid of (148 x resident CTAs) warps walking the item
+// table (profiles/r01_final.md: 97.5 % / 97.4 % of the measured HBM copy bandwidth).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -50,7 +51,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // or a fixed PTX instruction (no FMA contraction, no fast-math, no data-dependent branches),
 // so pass B recomputes bit-for-bit the u that pass A normed.  sqrt/rcp use the branch-free
 // MUFU approximations (<= 1-2 ulp; the IEEE-rounded sequences carry slow-path branches that
-// made the passes issue-bound, see profiles/r01_notes.md); u stays within ~4 ulp of the
+// made the passes issue-bound, see profiles/r01_baseline.md); u stays within ~4 ulp of the
 // correctly rounded fp32 value, far inside the 1e-5 contract.
 __device__ __forceinline__ float sqrt_approx(float x) {
     float y;
@@ -265,7 +266,9 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_a_pf_kernel(const __grid_
 
 // Pass A with a shared-memory ring for the gradient words (FUSED, NS >= 2): every lane
 // streams its own future gradient chunks (NS x 8 B per chunk, mostly remote) with cp.async,
-// P-1 U-blocks ahead of use, so NVLink latency is covered without holding registers.  A lane
+// PD-1 U-blocks ahead of use, so NVLink latency is covered without holding registers (tunable
+// LAMB_TUNE ring=3|4|6; not the default: 2 % slower than the register prefetch at D = 2,
+// profiles/r01/sweep_ring.jsonl — the limit there is shared HBM, not latency).  A lane
 // only ever reads back what it copied itself (wait_group makes its own copies visible), so no
 // warp synchronisation is needed.
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -613,8 +616,8 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 // A.flags[j] -> rank j's flag array (uint64[LAMB_MAX_RANKS]); slot i of rank j's array holds
 // the last epoch rank i announced to j.  Every rank runs the same sequence of barriers, so the
-// epoch counters agree.  A peer that does not arrive within 30 s sets *err (host-mapped) and
-// the kernel exits instead of hanging the GPU.
+// epoch counters agree.  A peer that does not arrive within timeout_ns (LAMB_BARRIER_TIMEOUT_MS,
+// per handle) sets *err (host-mapped) and the kernel exits instead of hanging the GPU.
 struct BarrierArgs {
     uint64_t* flags[LAMB_MAX_RANKS];
 };
