@@ -256,6 +256,16 @@ lamb_status lamb_checkpoint_wait(lamb_t h);
  * EINVAL: unreadable file, wrong magic/version, or a different parameter table. */
 lamb_status lamb_checkpoint_load(lamb_t h, const char* path, int64_t* step, void* stream);
 
+/* ---------------- self-check (§4.3 P:163-193 diagnostic tests) ----------------
+ * Device-side audit of this rank's state, e.g. before resuming on a replacement machine.
+ * counts[0]: shard entries with a non-finite w, m or v, or v < 0;
+ * counts[1]: own-slice params that differ from bf16_rne(w);
+ * counts[2]: nonzero w/m/v in the shard's padding;  counts[3]: nonzero grad/param padding
+ *            (a caller wrote outside a tensor view);
+ * counts[4]: peer mappings that read back as poisoned (FUSED).  All zero = healthy.
+ * Synchronises `stream`.  ESTATE: master not set. */
+lamb_status lamb_self_check(lamb_t h, int64_t counts[5], void* stream);
+
 /* ---------------- measurement (CUDA events, §5.1 P:21-35 style) ---------------- */
 #define LAMB_PH_BARRIER_IN 0   /* cross-GPU "grads ready" barrier (FUSED, D > 1) */
 #define LAMB_PH_PASS_A 1       /* a1+a2: (fused RS) + moments + update + partial norms */

@@ -74,6 +74,11 @@ struct lamb_ctx {
     int max_ctas = 0;   // SM budget of the streaming passes (0 = one full wave)
     bool diag_local_grads = false;   // LAMB_DIAG_LOCAL_GRADS: timing diagnostic, wrong results
     lamb::GroupConst* d_groups = nullptr;   // per-step group constants (prologue kernel)
+    // lamb_self_check: padding ranges and counters (built on first use)
+    bool pad_built = false;
+    int64_t *d_shard_pad = nullptr, *d_flat_pad = nullptr;
+    int64_t n_shard_pad = 0, n_flat_pad = 0;
+    unsigned long long* d_check = nullptr;
     // LAMB_FLAG_GRAPH
     cudaGraphExec_t graph_exec = nullptr;
     cudaStream_t cap_stream = nullptr;

@@ -140,7 +140,7 @@ static void free_ctx(lamb_ctx* h) {
     }
     void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->partials, h->segs, h->scale,
                     h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
-                    h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_clip_blocks, h->d_groups, h->d_tensor_off, h->d_numel,
+                    h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_clip_blocks, h->d_groups, h->d_shard_pad, h->d_flat_pad, h->d_check, h->d_tensor_off, h->d_numel,
                     h->d_shard_base, h->d_bucket_base, h->d_bucket_slice};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -961,6 +961,54 @@ extern "C" lamb_status lamb_sm_partition(int32_t device, int32_t lamb_sms, void*
     *lamb_stream = s1;
     *compute_stream = s2;
     if (got_sms) *got_sms = (int32_t)part.sm.smCount;
+    return LAMB_OK;
+}
+
+// ------------------------------------------------------------------ self-check (§4.3)
+// Padding ranges: shard positions not covered by a segment rounded up to 8 (w/m/v must stay 0)
+// and flat positions not covered by any tensor (grad/param must stay 0).  Built on first use.
+static lamb_status build_padding(lamb_ctx* h) {
+    if (h->pad_built) return LAMB_OK;
+    const Plan& p = h->plan;
+    std::vector<int64_t> sh, fl;
+    int64_t pos = 0;
+    for (int64_t k = 0; k < p.n_segments(); ++k) {
+        const int64_t soff = p.segments[4 * k + 1], len = p.segments[4 * k + 3];
+        if (soff > pos) sh.insert(sh.end(), {pos, soff});
+        pos = soff + len;   // [len, len8) is padding too: checked below as part of the gap
+    }
+    if (p.shard_size > pos) sh.insert(sh.end(), {pos, p.shard_size});
+    pos = 0;
+    for (int64_t i = 0; i < p.n_tensors(); ++i) {
+        if (p.tensor_off[i] > pos) fl.insert(fl.end(), {pos, p.tensor_off[i]});
+        pos = p.tensor_off[i] + p.numel[i];
+    }
+    if (p.flat_size > pos) fl.insert(fl.end(), {pos, p.flat_size});
+    CUDA_TRY(h, upload(&h->d_shard_pad, sh));
+    CUDA_TRY(h, upload(&h->d_flat_pad, fl));
+    h->n_shard_pad = (int64_t)sh.size() / 2;
+    h->n_flat_pad = (int64_t)fl.size() / 2;
+    CUDA_TRY(h, dalloc(&h->d_check, 5));
+    h->pad_built = true;
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_self_check(lamb_t h, int64_t counts[5], void* stream) {
+    if (!h || !counts) return fail(h, LAMB_EINVAL, "null argument");
+    if (!h->master_set) return fail(h, LAMB_ESTATE, "nothing to check: master not set");
+    cudaSetDevice(h->device);
+    lamb_status st = build_padding(h);
+    if (st != LAMB_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t* flags[LAMB_MAX_RANKS];
+    for (int j = 0; j < h->cfg.world_size; ++j) flags[j] = h->flags(j);
+    LAUNCH(h, lamb::launch_self_check(h->items, h->n_items, h->w, h->m, h->v, h->grad, h->param, h->d_shard_pad,
+                                      h->n_shard_pad, h->d_flat_pad, h->n_flat_pad, flags, h->cfg.world_size,
+                                      h->d_check, s));
+    unsigned long long c[5];
+    CUDA_TRY(h, cudaMemcpyAsync(c, h->d_check, sizeof(c), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    for (int k = 0; k < 5; ++k) counts[k] = (int64_t)c[k];
     return LAMB_OK;
 }
 

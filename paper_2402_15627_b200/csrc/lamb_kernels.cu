@@ -679,6 +679,77 @@ __global__ void cast_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* _
         dst[i] = __float2bfloat16_rn(src[i]);
 }
 
+// ------------------------------------------------------------ self-check (§4.3)
+// Audit of this rank's state: per item, fp32 w/m/v finite and v >= 0, own-slice params equal
+// bf16_rne(w); every padding range of the shard (w, m, v) and of the flat buffers (grad, param)
+// is exactly zero; each peer mapping readable.  Counts go to out[5] (atomics are fine here:
+// only counts, no floating-point reduction).
+__global__ void self_check_items_kernel(const Item* items, int64_t n_items, const float* w, const float* m,
+                                        const float* v, const __nv_bfloat16* param, unsigned long long* out) {
+    unsigned long long bad_nonfinite = 0, bad_param = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item I = items[it];
+        for (int c = threadIdx.x; c < I.n_chunk * 4; c += blockDim.x) {
+            const int64_t s = I.shard_off + c, f = I.flat_off + c;
+            const float ww = w[s], mm = m[s], vv = v[s];
+            if (!isfinite(ww) || !isfinite(mm) || !isfinite(vv) || vv < 0.f) ++bad_nonfinite;
+            const __nv_bfloat16 p = __float2bfloat16_rn(ww);
+            if (*reinterpret_cast<const uint16_t*>(&p) != *reinterpret_cast<const uint16_t*>(param + f)) ++bad_param;
+        }
+    }
+    if (bad_nonfinite) atomicAdd(out + 0, bad_nonfinite);
+    if (bad_param) atomicAdd(out + 1, bad_param);
+}
+
+// ranges[k] = {begin, end} in elements; kind 0: shard ranges (w/m/v), 1: flat ranges (grad/param)
+__global__ void self_check_padding_kernel(const int64_t* ranges, int64_t n_ranges, int kind, const float* w,
+                                          const float* m, const float* v, const __nv_bfloat16* grad,
+                                          const __nv_bfloat16* param, unsigned long long* out) {
+    unsigned long long bad = 0;
+    for (int64_t k = blockIdx.x; k < n_ranges; k += gridDim.x) {
+        for (int64_t e = ranges[2 * k] + threadIdx.x; e < ranges[2 * k + 1]; e += blockDim.x) {
+            if (kind == 0) {
+                if (w[e] != 0.f || m[e] != 0.f || v[e] != 0.f) ++bad;
+            } else {
+                const uint16_t g = *reinterpret_cast<const uint16_t*>(grad + e);
+                const uint16_t q = *reinterpret_cast<const uint16_t*>(param + e);
+                if (g != 0 || q != 0) ++bad;
+            }
+        }
+    }
+    if (bad) atomicAdd(out + 2 + kind, bad);
+}
+
+struct PeerArgs {
+    const uint64_t* flags[LAMB_MAX_RANKS];
+};
+__global__ void self_check_peers_kernel(const __grid_constant__ PeerArgs A, int world, unsigned long long* out) {
+    const int j = threadIdx.x;
+    if (j < world) {
+        uint64_t x;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(A.flags[j]) : "memory");
+        if (x == ~0ull) atomicAdd(out + 4, 1ull);   // an all-ones word = unreachable / poisoned mapping
+    }
+}
+
+cudaError_t launch_self_check(const Item* items, int64_t n_items, const float* w, const float* m, const float* v,
+                              const __nv_bfloat16* grad, const __nv_bfloat16* param, const int64_t* shard_pad,
+                              int64_t n_shard_pad, const int64_t* flat_pad, int64_t n_flat_pad,
+                              const uint64_t* const* peer_flags, int world, unsigned long long* out,
+                              cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, 5 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    if (n_items > 0) self_check_items_kernel<<<148 * 8, 256, 0, s>>>(items, n_items, w, m, v, param, out);
+    if (n_shard_pad > 0)
+        self_check_padding_kernel<<<148 * 4, 256, 0, s>>>(shard_pad, n_shard_pad, 0, w, m, v, grad, param, out);
+    if (n_flat_pad > 0)
+        self_check_padding_kernel<<<148 * 4, 256, 0, s>>>(flat_pad, n_flat_pad, 1, w, m, v, grad, param, out);
+    PeerArgs pa;
+    for (int j = 0; j < LAMB_MAX_RANKS; ++j) pa.flags[j] = j < world ? peer_flags[j] : nullptr;
+    self_check_peers_kernel<<<1, 32, 0, s>>>(pa, world, out);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ step prologue
 __global__ void prologue_kernel(const __grid_constant__ GroupTable T, int n, GroupConst* dst) {
     const int i = threadIdx.x;

@@ -114,6 +114,11 @@ struct GroupTable {
 };
 
 // Host launchers (lamb_kernels.cu).  `occ_grid` = persistent grid size.
+cudaError_t launch_self_check(const Item* items, int64_t n_items, const float* w, const float* m, const float* v,
+                              const __nv_bfloat16* grad, const __nv_bfloat16* param, const int64_t* shard_pad,
+                              int64_t n_shard_pad, const int64_t* flat_pad, int64_t n_flat_pad,
+                              const uint64_t* const* peer_flags, int world, unsigned long long* out,
+                              cudaStream_t s);
 cudaError_t launch_prologue(const GroupTable& t, int n_groups, GroupConst* dst, cudaStream_t s);
 cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int grid, cudaStream_t s);
 cudaError_t launch_pass_b(const StepParams& p, int ndst, int grid, cudaStream_t s);

@@ -89,6 +89,7 @@ _SIGS = {
     "lamb_step_bucket": (_st, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _vp]),
     "lamb_gather_bucket": (_st, [_vp, ctypes.c_int64, _vp]),
     "lamb_set_max_ctas": (_st, [_vp, ctypes.c_int32]),
+    "lamb_self_check": (_st, [_vp, _vp, _vp]),
     "lamb_sm_partition": (_st, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                 ctypes.POINTER(ctypes.c_int32)]),
     "lamb_destroy": (None, [_vp]),
@@ -274,6 +275,14 @@ class Lamb:
     def step_bucket(self, bucket: int, t: int, defer_ag: bool = False, stream=None) -> None:
         check(lamb_step_bucket(self.h, int(bucket), int(t), LAMB_BUCKET_DEFER_AG if defer_ag else 0,
                                self._stream(stream)), self.h)
+
+    def self_check(self) -> dict:
+        """lamb_self_check: device-side audit (§4.3); all counts zero = healthy."""
+        c = (ctypes.c_int64 * 5)()
+        check(lamb_self_check(self.h, c, self._stream(None)), self.h)
+        keys = ("nonfinite_state", "param_mismatch", "shard_padding_nonzero", "flat_padding_nonzero",
+                "peer_unreachable")
+        return dict(zip(keys, list(c)))
 
     def set_max_ctas(self, max_ctas: int) -> None:
         check(lamb_set_max_ctas(self.h, int(max_ctas)), self.h)

@@ -70,6 +70,8 @@ def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, chec
     dist.all_gather(hs, win)
     assert all(torch.equal(x, hs[0]) for x in hs), f"{name}: param buffers differ across ranks"
     n_strad = len(L.plan.straddlers)
+    if check_all_params:
+        assert all(v == 0 for v in L.self_check().values()), L.self_check()
     L.close()
     if rank == 0:
         print(f"[ok] {name} D={world} mode={mode} steps={steps} straddlers={n_strad} "

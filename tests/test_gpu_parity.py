@@ -494,3 +494,24 @@ def test_torch_optimizer_binding_end_to_end(lamb):
         pb = ordered[i].detach().reshape(-1)[toff:toff + ln].view(torch.int16).cpu().numpy().view(np.uint16)
         assert np.array_equal(pb, oracle.bf16_rne_bits(Wg[soff:soff + ln].astype(np.float64)))
     opt.L.close()
+
+
+def test_self_check_detects_corruption(lamb):
+    """lamb_self_check (§4.3-style diagnostic): healthy state reads all-zero; a NaN in
+    m, a stale param, nonzero shard padding and a write outside a tensor view are each found."""
+    wl = W.toy()
+    L = run_gpu(wl, steps=2)
+    assert all(v == 0 for v in L.self_check().values())
+    tail = int(L.plan.tensor_off[0]) + wl.tensors[0].numel          # padding after tensor 0? (3072 is 8-aligned)
+    flat_pad = int(L.plan.tensor_off[1]) + wl.tensors[1].numel      # t1 = 48 elements -> next start 3120: no gap
+    flat_pad = int(L.plan.tensor_off[2]) + wl.tensors[2].numel      # end of t2 .. flat_size is padding
+    L.grad_buffer()[flat_pad + 3] = 1.0
+    L.state_buffer(lamb.LAMB_BUF_M)[17] = float("nan")
+    L.param_buffer()[5] = 123.0
+    L.state_buffer(lamb.LAMB_BUF_V)[L.plan.shard_size - 1] = 1.0   # last shard element is padding
+    torch.cuda.synchronize()
+    c = L.self_check()
+    assert c["nonfinite_state"] >= 1 and c["param_mismatch"] >= 1
+    assert c["shard_padding_nonzero"] >= 1 and c["flat_padding_nonzero"] >= 1
+    assert c["peer_unreachable"] == 0
+    L.close()
