@@ -356,6 +356,117 @@ __global__ void __launch_bounds__(kThreads, 2) pass_a_ring_kernel(const __grid_c
     }
 }
 
+// ------------------------------------------------------------ pass A, TMA variant (D = 1)
+// One producer warp stages whole items (g 8 B, m/v/w 16 B per 4-element chunk) into a 3-stage
+// shared-memory ring with 1-D bulk copies (cp.async.bulk, TMA engine; mbarrier complete_tx);
+// 8 consumer warps compute from shared memory and store m, v with 16 B STGs.  Tunable
+// (LAMB_TUNE tma=1) against the LDG kernel.
+constexpr int kTmaStages = 3;
+constexpr int kTmaConsumers = 256;
+constexpr int kTmaItem = (int)kItemElems;   // elements per stage (one item)
+struct TmaStage {
+    float4 m[kTmaItem / 4], v[kTmaItem / 4], w[kTmaItem / 4];
+    uint2 g[kTmaItem / 4];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const __grid_constant__ StepParams P) {
+    extern __shared__ __align__(128) unsigned char tma_smem[];
+    TmaStage* st = reinterpret_cast<TmaStage*>(tma_smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem + sizeof(TmaStage) * kTmaStages);
+    uint64_t* empty = full + kTmaStages;
+    __shared__ double red_w[kTmaConsumers / 32], red_u[kTmaConsumers / 32];
+    const int tid = threadIdx.x;
+    if (P.clip && P.clip->skip) return;
+    if (tid == 0) {
+        for (int k = 0; k < kTmaStages; ++k) {
+            mbar_init(full + k, 1);
+            mbar_init(empty + k, kTmaConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t first = P.item_begin + blockIdx.x, stride = gridDim.x;
+    if (tid >= kTmaConsumers) {
+        // ---------------- producer warp (one elected lane issues the bulk copies)
+        if (tid == kTmaConsumers) {
+            int k = 0;
+            uint32_t phase = 0;
+            for (int64_t it = first; it < P.item_end; it += stride) {
+                mbar_wait(empty + k, phase ^ 1);
+                const Item I = P.items[it];
+                const uint32_t nf = (uint32_t)I.n_chunk * 16u, ng = (uint32_t)I.n_chunk * 8u;
+                mbar_expect_tx(full + k, 3 * nf + ng);
+                bulk_g2s(st[k].m, P.m + I.shard_off, nf, full + k);
+                bulk_g2s(st[k].v, P.v + I.shard_off, nf, full + k);
+                bulk_g2s(st[k].w, P.w + I.shard_off, nf, full + k);
+                bulk_g2s(st[k].g, P.gsrc[0] + I.flat_off, ng, full + k);
+                if (++k == kTmaStages) { k = 0; phase ^= 1; }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers
+    const float gs = P.clip ? P.clip->gs : P.grad_scale;
+    const int lane = tid & 31, warp = tid >> 5;
+    int k = 0;
+    uint32_t phase = 0;
+    for (int64_t it = first; it < P.item_end; it += stride) {
+        const Item I = P.items[it];
+        const GroupConst G = P.groups[I.group];
+        mbar_wait(full + k, phase);
+        float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
+        float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
+        float sw = 0.f, su = 0.f;
+        for (int c = tid; c < I.n_chunk; c += kTmaConsumers) {
+            const uint2 r = st[k].g[c];
+            float4 m = st[k].m[c], v = st[k].v[c];
+            const float4 w = st[k].w[c];
+            chunk_a(make_float4(bf_lo(r.x), bf_hi(r.x), bf_lo(r.y), bf_hi(r.y)), m, v, w, gs, G, sw, su);
+            __stcs(mp + c, m);
+            __stcs(vp + c, v);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + k);   // this warp is done with the stage
+        double dw = warp_sum((double)sw), du = warp_sum((double)su);
+        if (lane == 0) {
+            red_w[warp] = dw;
+            red_u[warp] = du;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));   // consumers only
+        if (tid == 0) {
+            double a = 0.0, b = 0.0;
+            for (int q = 0; q < kTmaConsumers / 32; ++q) {
+                a += red_w[q];
+                b += red_u[q];
+            }
+            P.partials[it] = make_double2(a, b);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
+        if (++k == kTmaStages) { k = 0; phase ^= 1; }
+    }
+}
+
 // ------------------------------------------------------------ pass B
 __device__ __forceinline__ uint2 chunk_b(const float4 m, const float4 v, float4& w, float scale,
                                          const GroupConst& G) {
@@ -763,12 +874,13 @@ struct Tune {
     int ua = 4, ma = 2, ub = 4, mb = 2;
     int pf = 1, upf = 4;   // FUSED (NS >= 2): prefetching pass A (U = 4 for NS = 2, else 2; r01 sweep)
     int ring = 0;          // FUSED (NS >= 2): cp.async smem ring of this depth (0 = off)
+    int tma = 0;           // D = 1: TMA bulk-copy pass A (0 = off)
 };
 static Tune g_tune = [] {
     Tune t;
     if (const char* e = getenv("LAMB_TUNE")) {
-        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d,ring=%d", &t.ua, &t.ma, &t.ub, &t.mb, &t.pf, &t.upf,
-               &t.ring);
+        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d,ring=%d,tma=%d", &t.ua, &t.ma, &t.ub, &t.mb, &t.pf,
+               &t.upf, &t.ring, &t.tma);
     }
     return t;
 }();
@@ -796,9 +908,28 @@ static cudaError_t pass_a_ring(const StepParams& p, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+static cudaError_t pass_a_tma(const StepParams& p, int device, cudaStream_t s) {
+    const size_t smem = sizeof(TmaStage) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
+    static int grid = [&] {
+        cudaFuncSetAttribute(pass_a_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        return sms;   // one CTA per SM (the ring uses ~170 KB of shared memory)
+    }();
+    pass_a_tma_kernel<<<grid, kTmaConsumers + 32, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <int NS>
 static cudaError_t pass_a_ns(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
+    if constexpr (NS == 1) {
+        if (t.tma) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            return pass_a_tma(p, dev, s);
+        }
+    }
     if constexpr (NS >= 2 && NS <= 4) {
         if (t.ring == 3) return pass_a_ring<NS, 4, 3>(p, grid, s);
         if (t.ring == 4) return pass_a_ring<NS, 4, 4>(p, grid, s);
