@@ -522,6 +522,68 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_b_kernel(const __grid_con
     if constexpr (ND > 1) __threadfence_system();   // peer stores visible before the barrier
 }
 
+// ------------------------------------------------------------ pass B, TMA variant (D = 1)
+// Same ring as pass A's TMA variant: the producer stages m, v, w of an item; consumers recompute
+// u, store w (16 B) and p (8 B) with streaming STGs.
+struct TmaStageB {
+    float4 m[kTmaItem / 4], v[kTmaItem / 4], w[kTmaItem / 4];
+};
+
+__global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const __grid_constant__ StepParams P) {
+    extern __shared__ __align__(128) unsigned char tma_smem_b[];
+    TmaStageB* st = reinterpret_cast<TmaStageB*>(tma_smem_b);
+    uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem_b + sizeof(TmaStageB) * kTmaStages);
+    uint64_t* empty = full + kTmaStages;
+    const int tid = threadIdx.x;
+    if (P.clip && P.clip->skip) return;
+    if (tid == 0) {
+        for (int k = 0; k < kTmaStages; ++k) {
+            mbar_init(full + k, 1);
+            mbar_init(empty + k, kTmaConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t first = P.item_begin + blockIdx.x, stride = gridDim.x;
+    if (tid >= kTmaConsumers) {
+        if (tid == kTmaConsumers) {
+            int k = 0;
+            uint32_t phase = 0;
+            for (int64_t it = first; it < P.item_end; it += stride) {
+                mbar_wait(empty + k, phase ^ 1);
+                const Item I = P.items[it];
+                const uint32_t nf = (uint32_t)I.n_chunk * 16u;
+                mbar_expect_tx(full + k, 3 * nf);
+                bulk_g2s(st[k].m, P.m + I.shard_off, nf, full + k);
+                bulk_g2s(st[k].v, P.v + I.shard_off, nf, full + k);
+                bulk_g2s(st[k].w, P.w + I.shard_off, nf, full + k);
+                if (++k == kTmaStages) { k = 0; phase ^= 1; }
+            }
+        }
+        return;
+    }
+    const int lane = tid & 31;
+    int k = 0;
+    uint32_t phase = 0;
+    for (int64_t it = first; it < P.item_end; it += stride) {
+        const Item I = P.items[it];
+        const GroupConst G = P.groups[I.group];
+        const float scale = P.scale[I.tensor];
+        mbar_wait(full + k, phase);
+        float4* __restrict__ wp = reinterpret_cast<float4*>(P.w + I.shard_off);
+        uint2* __restrict__ pp = reinterpret_cast<uint2*>(P.pdst[0] + I.flat_off);
+        for (int c = tid; c < I.n_chunk; c += kTmaConsumers) {
+            float4 w = st[k].w[c];
+            const uint2 pb = chunk_b(st[k].m[c], st[k].v[c], w, scale, G);
+            __stcs(wp + c, w);
+            __stcs(pp + c, pb);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + k);
+        if (++k == kTmaStages) { k = 0; phase ^= 1; }
+    }
+}
+
 // ------------------------------------------------------------ pre-step (NEXT #3)
 // Sum of squares of the reduced gradient sums per item (fp32 block partials -> fp64, as the
 // norms), optionally materialising the fp32 sums into g32_out (FUSED, D > 1: the reduce-scatter
@@ -874,7 +936,7 @@ struct Tune {
     int ua = 4, ma = 2, ub = 4, mb = 2;
     int pf = 1, upf = 4;   // FUSED (NS >= 2): prefetching pass A (U = 4 for NS = 2, else 2; r01 sweep)
     int ring = 0;          // FUSED (NS >= 2): cp.async smem ring of this depth (0 = off)
-    int tma = 0;           // D = 1: TMA bulk-copy pass A (0 = off)
+    int tma = 1;           // D = 1: TMA bulk-copy passes (r01: pass A 98.1 % -> 99.9 % of HBM)
 };
 static Tune g_tune = [] {
     Tune t;
@@ -908,15 +970,25 @@ static cudaError_t pass_a_ring(const StepParams& p, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-static cudaError_t pass_a_tma(const StepParams& p, int device, cudaStream_t s) {
-    const size_t smem = sizeof(TmaStage) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
-    static int grid = [&] {
-        cudaFuncSetAttribute(pass_a_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int sms = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-        return sms;   // one CTA per SM (the ring uses ~170 KB of shared memory)
+// one CTA per SM (the ring uses ~170 KB of shared memory); `grid` (the SM budget) caps it
+static int tma_grid(int grid) {
+    static const int sms = [] {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
     }();
-    pass_a_tma_kernel<<<grid, kTmaConsumers + 32, smem, s>>>(p);
+    return grid < sms ? grid : sms;
+}
+
+static cudaError_t pass_a_tma(const StepParams& p, int grid, cudaStream_t s) {
+    const size_t smem = sizeof(TmaStage) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
+    static const bool attr = [&] {
+        cudaFuncSetAttribute(pass_a_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+    }();
+    (void)attr;
+    pass_a_tma_kernel<<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -924,11 +996,7 @@ template <int NS>
 static cudaError_t pass_a_ns(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
     if constexpr (NS == 1) {
-        if (t.tma) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            return pass_a_tma(p, dev, s);
-        }
+        if (t.tma) return pass_a_tma(p, grid, s);
     }
     if constexpr (NS >= 2 && NS <= 4) {
         if (t.ring == 3) return pass_a_ring<NS, 4, 3>(p, grid, s);
@@ -971,9 +1039,23 @@ static cudaError_t pass_b_v(const StepParams& p, int grid, cudaStream_t s) {
     pass_b_kernel<ND, U, M><<<grid, kThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
+static cudaError_t pass_b_tma(const StepParams& p, int grid, cudaStream_t s) {
+    const size_t smem = sizeof(TmaStageB) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
+    static const bool attr = [&] {
+        cudaFuncSetAttribute(pass_b_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+    }();
+    (void)attr;
+    pass_b_tma_kernel<<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <int ND>
 static cudaError_t pass_b_nd(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
+    if constexpr (ND == 1) {
+        if (t.tma) return pass_b_tma(p, grid, s);
+    }
     if (t.ub == 2 && t.mb == 4) return pass_b_v<ND, 2, 4>(p, grid, s);
     if (t.ub == 2 && t.mb == 3) return pass_b_v<ND, 2, 3>(p, grid, s);
     if (t.ub == 4 && t.mb == 3) return pass_b_v<ND, 4, 3>(p, grid, s);
