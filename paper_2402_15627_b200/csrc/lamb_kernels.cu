@@ -364,10 +364,13 @@ __global__ void __launch_bounds__(kThreads, 2) pass_a_ring_kernel(const __grid_c
 constexpr int kTmaStages = 3;
 constexpr int kTmaConsumers = 256;
 constexpr int kTmaItem = (int)kItemElems;   // elements per stage (one item)
+template <int NS>
 struct TmaStage {
     float4 m[kTmaItem / 4], v[kTmaItem / 4], w[kTmaItem / 4];
-    uint2 g[kTmaItem / 4];
+    uint2 g[NS][kTmaItem / 4];
 };
+template <int NS>
+__host__ __device__ constexpr int tma_stages_a() { return NS <= 2 ? 3 : 2; }   // fits 227 KB of shared memory
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
@@ -390,16 +393,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// NS = 1: D = 1 (local gradients); NS = D >= 2: the fused reduce-scatter — the bulk copies pull
+// each rank's gradient slice of the item (over NVLink for peers) into shared memory.
+template <int NS>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const __grid_constant__ StepParams P) {
+    constexpr int S = tma_stages_a<NS>();
     extern __shared__ __align__(128) unsigned char tma_smem[];
-    TmaStage* st = reinterpret_cast<TmaStage*>(tma_smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem + sizeof(TmaStage) * kTmaStages);
-    uint64_t* empty = full + kTmaStages;
+    TmaStage<NS>* st = reinterpret_cast<TmaStage<NS>*>(tma_smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem + sizeof(TmaStage<NS>) * S);
+    uint64_t* empty = full + S;
     __shared__ double red_w[kTmaConsumers / 32], red_u[kTmaConsumers / 32];
     const int tid = threadIdx.x;
     if (P.clip && P.clip->skip) return;
     if (tid == 0) {
-        for (int k = 0; k < kTmaStages; ++k) {
+        for (int k = 0; k < S; ++k) {
             mbar_init(full + k, 1);
             mbar_init(empty + k, kTmaConsumers / 32);
         }
@@ -416,12 +423,13 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
                 mbar_wait(empty + k, phase ^ 1);
                 const Item I = P.items[it];
                 const uint32_t nf = (uint32_t)I.n_chunk * 16u, ng = (uint32_t)I.n_chunk * 8u;
-                mbar_expect_tx(full + k, 3 * nf + ng);
+                mbar_expect_tx(full + k, 3 * nf + NS * ng);
+#pragma unroll
+                for (int j = 0; j < NS; ++j) bulk_g2s(st[k].g[j], P.gsrc[j] + I.flat_off, ng, full + k);
                 bulk_g2s(st[k].m, P.m + I.shard_off, nf, full + k);
                 bulk_g2s(st[k].v, P.v + I.shard_off, nf, full + k);
                 bulk_g2s(st[k].w, P.w + I.shard_off, nf, full + k);
-                bulk_g2s(st[k].g, P.gsrc[0] + I.flat_off, ng, full + k);
-                if (++k == kTmaStages) { k = 0; phase ^= 1; }
+                if (++k == S) { k = 0; phase ^= 1; }
             }
         }
         return;
@@ -439,16 +447,18 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
         float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
         float sw = 0.f, su = 0.f;
         for (int c = tid; c < I.n_chunk; c += kTmaConsumers) {
-            const uint2 r = st[k].g[c];
+            uint2 raw[NS];
+#pragma unroll
+            for (int j = 0; j < NS; ++j) raw[j] = st[k].g[j][c];
             float4 m = st[k].m[c], v = st[k].v[c];
             const float4 w = st[k].w[c];
-            chunk_a(make_float4(bf_lo(r.x), bf_hi(r.x), bf_lo(r.y), bf_hi(r.y)), m, v, w, gs, G, sw, su);
+            chunk_a(sum_raw<NS>(raw), m, v, w, gs, G, sw, su);   // fp32 sum in rank order (Z11)
             __stcs(mp + c, m);
             __stcs(vp + c, v);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + k);   // this warp is done with the stage
-        double dw = warp_sum((double)sw), du = warp_sum((double)su);
+        const double dw = warp_sum((double)sw), du = warp_sum((double)su);
         if (lane == 0) {
             red_w[warp] = dw;
             red_u[warp] = du;
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
             P.partials[it] = make_double2(a, b);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
-        if (++k == kTmaStages) { k = 0; phase ^= 1; }
+        if (++k == S) { k = 0; phase ^= 1; }
     }
 }
 
@@ -529,6 +539,7 @@ struct TmaStageB {
     float4 m[kTmaItem / 4], v[kTmaItem / 4], w[kTmaItem / 4];
 };
 
+template <int ND>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const __grid_constant__ StepParams P) {
     extern __shared__ __align__(128) unsigned char tma_smem_b[];
     TmaStageB* st = reinterpret_cast<TmaStageB*>(tma_smem_b);
@@ -571,17 +582,18 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const
         const float scale = P.scale[I.tensor];
         mbar_wait(full + k, phase);
         float4* __restrict__ wp = reinterpret_cast<float4*>(P.w + I.shard_off);
-        uint2* __restrict__ pp = reinterpret_cast<uint2*>(P.pdst[0] + I.flat_off);
         for (int c = tid; c < I.n_chunk; c += kTmaConsumers) {
             float4 w = st[k].w[c];
             const uint2 pb = chunk_b(st[k].m[c], st[k].v[c], w, scale, G);
             __stcs(wp + c, w);
-            __stcs(pp + c, pb);
+#pragma unroll
+            for (int j = 0; j < ND; ++j) __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c, pb);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + k);
         if (++k == kTmaStages) { k = 0; phase ^= 1; }
     }
+    if constexpr (ND > 1) __threadfence_system();   // peer stores visible before the barrier
 }
 
 // ------------------------------------------------------------ pre-step (NEXT #3)
@@ -937,12 +949,13 @@ struct Tune {
     int pf = 1, upf = 4;   // FUSED (NS >= 2): prefetching pass A (U = 4 for NS = 2, else 2; r01 sweep)
     int ring = 0;          // FUSED (NS >= 2): cp.async smem ring of this depth (0 = off)
     int tma = 1;           // D = 1: TMA bulk-copy passes (r01: pass A 98.1 % -> 99.9 % of HBM)
+    int tma_multi = 0;     // FUSED D >= 2: TMA passes (peer gradient slices pulled by bulk copies)
 };
 static Tune g_tune = [] {
     Tune t;
     if (const char* e = getenv("LAMB_TUNE")) {
-        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d,ring=%d,tma=%d", &t.ua, &t.ma, &t.ub, &t.mb, &t.pf,
-               &t.upf, &t.ring, &t.tma);
+        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d,ring=%d,tma=%d,tmam=%d", &t.ua, &t.ma, &t.ub, &t.mb,
+               &t.pf, &t.upf, &t.ring, &t.tma, &t.tma_multi);
     }
     return t;
 }();
@@ -981,22 +994,23 @@ static int tma_grid(int grid) {
     return grid < sms ? grid : sms;
 }
 
+template <int NS>
 static cudaError_t pass_a_tma(const StepParams& p, int grid, cudaStream_t s) {
-    const size_t smem = sizeof(TmaStage) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
+    const size_t smem = sizeof(TmaStage<NS>) * tma_stages_a<NS>() + 2 * tma_stages_a<NS>() * sizeof(uint64_t);
     static const bool attr = [&] {
-        cudaFuncSetAttribute(pass_a_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(pass_a_tma_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return true;
     }();
     (void)attr;
-    pass_a_tma_kernel<<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
+    pass_a_tma_kernel<NS><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 template <int NS>
 static cudaError_t pass_a_ns(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
-    if constexpr (NS == 1) {
-        if (t.tma) return pass_a_tma(p, grid, s);
+    if constexpr (NS >= 1) {
+        if (NS == 1 ? t.tma : t.tma_multi) return pass_a_tma<NS>(p, grid, s);
     }
     if constexpr (NS >= 2 && NS <= 4) {
         if (t.ring == 3) return pass_a_ring<NS, 4, 3>(p, grid, s);
@@ -1039,23 +1053,22 @@ static cudaError_t pass_b_v(const StepParams& p, int grid, cudaStream_t s) {
     pass_b_kernel<ND, U, M><<<grid, kThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
+template <int ND>
 static cudaError_t pass_b_tma(const StepParams& p, int grid, cudaStream_t s) {
     const size_t smem = sizeof(TmaStageB) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
     static const bool attr = [&] {
-        cudaFuncSetAttribute(pass_b_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(pass_b_tma_kernel<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return true;
     }();
     (void)attr;
-    pass_b_tma_kernel<<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
+    pass_b_tma_kernel<ND><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 template <int ND>
 static cudaError_t pass_b_nd(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
-    if constexpr (ND == 1) {
-        if (t.tma) return pass_b_tma(p, grid, s);
-    }
+    if (ND == 1 ? t.tma : t.tma_multi) return pass_b_tma<ND>(p, grid, s);
     if (t.ub == 2 && t.mb == 4) return pass_b_v<ND, 2, 4>(p, grid, s);
     if (t.ub == 2 && t.mb == 3) return pass_b_v<ND, 2, 3>(p, grid, s);
     if (t.ub == 4 && t.mb == 3) return pass_b_v<ND, 4, 3>(p, grid, s);
