@@ -27,13 +27,13 @@ import workloads as W  # noqa: E402
 METRIC = "LAMB params updated/sec & step ms at 1/2/4/8 B200; % HBM roofline"
 UNIT = "params/s"
 FALLBACK_HBM_GBS = 6650.0
-NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md measured peer copy per direction (context)
-# Per-GPU in-bound NVLink bandwidth of an all-to-all where every GPU pulls (loads) from / pushes
-# (stores) to every peer at once — the shape of the fused reduce-scatter (pass A) and
-# all-gather (pass B).  Measured on this pool with tools/p2p_bench.cu, 16 B per lane, D = 2 and
-# 4 (profiles/r01/p2p_all2all_D*.json): pull 624-633 GB/s, push 695-700 GB/s.
-NVLINK_PULL_GBS = 633.0
-NVLINK_PUSH_GBS = 700.0
+# NVLink roofline for the fused passes: B200_PROFILING.md prescribes "bytes that must cross
+# NVLink / link bandwidth, the measured 770 GB/s per direction per GPU".  (Context: an LDG-based
+# all-to-all on this pool reaches 633 GB/s pull / 700 GB/s push per GPU, tools/p2p_bench.cu,
+# profiles/r01/p2p_all2all_D*.json; the TMA pass A already pulls ~670 GB/s.)
+NVLINK_PEER_GBS = 770.0
+NVLINK_PULL_GBS = NVLINK_PEER_GBS
+NVLINK_PUSH_GBS = NVLINK_PEER_GBS
 
 
 def parse():
@@ -311,7 +311,7 @@ def main():
         roof = {"bound": "nvlink", "kernel": dom["kernel"], "achieved": dom["nvlink_GBps"],
                 "peak": dom["nvlink_peak"], "unit": "GB/s", "frac": dom["nvlink_frac"],
                 "traffic": traffic,
-                "peak_source": "measured all-to-all per-GPU in-bound NVLink (tools/p2p_bench.cu)"}
+                "peak_source": "B200_PROFILING.md measured peer copy, 770 GB/s per direction per GPU"}
     else:
         roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["GBps"], "peak": hbm,
                 "unit": "GB/s", "frac": dom["hbm_frac"], "traffic": traffic, "peak_source": hbm_src}

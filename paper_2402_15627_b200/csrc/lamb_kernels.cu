@@ -949,7 +949,8 @@ struct Tune {
     int pf = 1, upf = 4;   // FUSED (NS >= 2): prefetching pass A (U = 4 for NS = 2, else 2; r01 sweep)
     int ring = 0;          // FUSED (NS >= 2): cp.async smem ring of this depth (0 = off)
     int tma = 1;           // D = 1: TMA bulk-copy passes (r01: pass A 98.1 % -> 99.9 % of HBM)
-    int tma_multi = 0;     // FUSED D >= 2: TMA passes (peer gradient slices pulled by bulk copies)
+    int tma_multi = 1;     // FUSED D >= 2: TMA passes (peer gradient slices pulled by bulk copies;
+                           // r01: step -4.1 % at D = 2, -3.7 % at D = 4, profiles/r01/sweep_tma.jsonl)
 };
 static Tune g_tune = [] {
     Tune t;
