@@ -25,6 +25,7 @@
 #define LAMB_H_
 
 #include <stdint.h>
+#include <stddef.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -124,6 +125,25 @@ lamb_status lamb_get_unique_id(uint8_t id[LAMB_UNIQUE_ID_BYTES]);
 lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors, const lamb_group* groups,
                         int32_t n_groups, const lamb_config* cfg,
                         const uint8_t id[LAMB_UNIQUE_ID_BYTES], lamb_t* out);
+
+/* Host all-gather supplied by the caller (e.g. over its torch.distributed process group):
+ * every rank passes `bytes` bytes in `send`; on return `recv` holds rank j's bytes at offset
+ * j * bytes for every j in [0, D).  Returns 0 on success.  Called only during
+ * lamb_create_with_allgather, on the calling thread, the same number of times on every rank. */
+typedef int (*lamb_allgather_fn)(const void* send, void* recv, size_t bytes, void* user);
+
+/* COLLECTIVE.  lamb_create for LAMB_COMM_FUSED without an NCCL communicator: the table/config
+ * hash and the CUDA-IPC handles of every rank's grad/param/sync buffers are exchanged through
+ * `allgather` (§3.2 P:312-317 needs only the RS/AG data paths, which FUSED runs in the
+ * pass kernels over peer memory; NCCL there serves only as bootstrap).  Ranks may share a
+ * device: D processes on fewer GPUs time-slice it, which exercises the D-rank kernels and
+ * protocol on any box (tests; not a performance configuration).  Everything else as
+ * lamb_create.  EINVAL: allgather NULL, D > 1 with comm_mode != LAMB_COMM_FUSED, the callback
+ * returned non-zero, or the lamb_create conditions. */
+lamb_status lamb_create_with_allgather(const lamb_tensor* tensors, int64_t n_tensors,
+                                       const lamb_group* groups, int32_t n_groups,
+                                       const lamb_config* cfg, lamb_allgather_fn allgather, void* user,
+                                       lamb_t* out);
 
 /* COLLECTIVE, asynchronous, stream-ordered on `stream`.  Gradients are read from the
  * library grad buffer (lamb_buffer(LAMB_BUF_GRAD)) — every rank holds its full flat bf16

@@ -235,7 +235,21 @@ extern "C" lamb_status lamb_checkpoint_load(lamb_t h, const char* path, int64_t*
         CUDA_TRY(h, lamb::launch_cast_to_bf16(h->w + p.shard_base[b], h->param + base + (int64_t)p.rank * sl, sl, s));
         ++h->launches;
     }
-    if (p.world > 1) {
+    if (p.world > 1 && h->cfg.comm_mode == LAMB_COMM_FUSED) {
+        // FUSED: every rank's own slices are cast -> barrier -> pull the peers' slices over
+        // NVLink -> barrier (no rank rewrites its slices while a peer may still read them)
+        uint64_t* flags[LAMB_MAX_RANKS];
+        for (int j = 0; j < p.world; ++j) flags[j] = h->flags(j);
+        CUDA_TRY(h, lamb::launch_barrier(flags, h->epoch(), p.rank, p.world, h->err_flag_dev, s, h->barrier_timeout_ns));
+        for (int64_t b = 0; b < p.n_buckets(); ++b) {
+            const int64_t base = p.buckets[4 * b], sl = p.buckets[4 * b + 1] / p.world;
+            CUDA_TRY(h, lamb::launch_gather(const_cast<const __nv_bfloat16* const*>(h->peer_param), h->param, base,
+                                            sl, p.world, p.rank, s));
+            ++h->launches;
+        }
+        CUDA_TRY(h, lamb::launch_barrier(flags, h->epoch(), p.rank, p.world, h->err_flag_dev, s, h->barrier_timeout_ns));
+        h->launches += 2;
+    } else if (p.world > 1) {
         NCCL_TRY(h, ncclGroupStart());
         for (int64_t b = 0; b < p.n_buckets(); ++b) {
             const int64_t base = p.buckets[4 * b], sl = p.buckets[4 * b + 1] / p.world;

@@ -57,8 +57,10 @@ struct lamb_ctx {
     __nv_bfloat16* peer_grad[LAMB_MAX_RANKS] = {};
     __nv_bfloat16* peer_param[LAMB_MAX_RANKS] = {};
     char* peer_sync[LAMB_MAX_RANKS] = {};
-    // NCCL
+    // NCCL (null in FUSED mode created by lamb_create_with_allgather: the step needs no NCCL)
     ncclComm_t comm = nullptr;
+    lamb_allgather_fn host_ag = nullptr;   // bootstrap all-gather, set only inside lamb_create_*
+    void* host_ag_user = nullptr;
     cudaStream_t comm_stream = nullptr;
     float* g32 = nullptr;          // NCCL mode: reduced fp32 grad shard
     float* up32[2] = {nullptr, nullptr};   // NCCL mode: upcast staging, 2 buckets

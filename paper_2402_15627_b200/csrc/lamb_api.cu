@@ -247,11 +247,32 @@ static lamb_status build_tables(lamb_ctx* h) {
     return LAMB_OK;
 }
 
+// Bootstrap exchange: every rank contributes `bytes` bytes, `all` receives D * bytes in rank
+// order.  Through NCCL (device staging) when the handle has a communicator, else through the
+// caller's host all-gather (lamb_create_with_allgather).
+static lamb_status bootstrap_allgather(lamb_ctx* h, const void* mine, void* all, size_t bytes) {
+    const int D = h->cfg.world_size;
+    if (h->host_ag) {
+        if (h->host_ag(mine, all, bytes, h->host_ag_user) != 0)
+            return fail(h, LAMB_EINVAL, "lamb_create: the caller's all-gather failed");
+        return LAMB_OK;
+    }
+    char* dbuf = nullptr;
+    CUDA_TRY(h, cudaMalloc(&dbuf, bytes * (D + 1)));
+    CUDA_TRY(h, cudaMemcpy(dbuf + bytes * D, mine, bytes, cudaMemcpyHostToDevice));
+    NCCL_TRY(h, ncclAllGather(dbuf + bytes * D, dbuf, bytes, ncclChar, h->comm, 0));
+    CUDA_TRY(h, cudaMemcpy(all, dbuf, bytes * D, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    return LAMB_OK;
+}
+
 static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
     const int D = h->cfg.world_size, r = h->cfg.rank;
-    ncclUniqueId u;
-    memcpy(&u, id, sizeof(u));
-    NCCL_TRY(h, ncclCommInitRank(&h->comm, D, u, r));
+    if (!h->host_ag) {
+        ncclUniqueId u;
+        memcpy(&u, id, sizeof(u));
+        NCCL_TRY(h, ncclCommInitRank(&h->comm, D, u, r));
+    }
     {
         // collective-misuse check: every rank must pass the same tables and config (except
         // rank/device) — a 64-bit FNV-1a hash of them is all-gathered and compared
@@ -266,13 +287,9 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
         const int64_t cfgv[4] = {h->cfg.world_size, h->cfg.comm_mode, h->plan.cap, (int64_t)h->cfg.flags};
         mix(cfgv, sizeof(cfgv));
         mix(&h->cfg.grad_scale, sizeof(float));
-        uint64_t* dh = nullptr;
-        CUDA_TRY(h, cudaMalloc(&dh, 8 * (D + 1)));
-        CUDA_TRY(h, cudaMemcpy(dh + D, &hv, 8, cudaMemcpyHostToDevice));
-        NCCL_TRY(h, ncclAllGather(dh + D, dh, 1, ncclUint64, h->comm, 0));
         std::vector<uint64_t> all(D);
-        CUDA_TRY(h, cudaMemcpy(all.data(), dh, 8 * D, cudaMemcpyDeviceToHost));
-        cudaFree(dh);
+        lamb_status st = bootstrap_allgather(h, &hv, all.data(), sizeof(hv));
+        if (st != LAMB_OK) return st;
         for (int j = 0; j < D; ++j)
             if (all[j] != hv)
                 return fail(h, LAMB_EINVAL, "lamb_create: rank " + std::to_string(j) +
@@ -289,14 +306,11 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
     CUDA_TRY(h, cudaIpcGetMemHandle(&mine[0], h->grad));
     CUDA_TRY(h, cudaIpcGetMemHandle(&mine[1], h->param));
     CUDA_TRY(h, cudaIpcGetMemHandle(&mine[2], h->sync));
-    const size_t hb = sizeof(mine);
-    char* dbuf = nullptr;
-    CUDA_TRY(h, cudaMalloc(&dbuf, hb * (D + 1)));
-    CUDA_TRY(h, cudaMemcpy(dbuf + hb * D, mine, hb, cudaMemcpyHostToDevice));
-    NCCL_TRY(h, ncclAllGather(dbuf + hb * D, dbuf, hb, ncclChar, h->comm, 0));
     std::vector<cudaIpcMemHandle_t> all(3 * D);
-    CUDA_TRY(h, cudaMemcpy(all.data(), dbuf, hb * D, cudaMemcpyDeviceToHost));
-    cudaFree(dbuf);
+    {
+        lamb_status st = bootstrap_allgather(h, mine, all.data(), sizeof(mine));
+        if (st != LAMB_OK) return st;
+    }
     for (int j = 0; j < D; ++j) {
         if (j == r) continue;
         void* p = nullptr;
@@ -308,17 +322,19 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
         h->peer_sync[j] = static_cast<char*>(p);
     }
     // make sure every rank has mapped everything before the first step
-    int* one = nullptr;
-    CUDA_TRY(h, cudaMalloc(&one, sizeof(int)));
-    NCCL_TRY(h, ncclAllReduce(one, one, 1, ncclInt, ncclSum, h->comm, 0));
     CUDA_TRY(h, cudaDeviceSynchronize());
-    cudaFree(one);
+    {
+        const uint8_t ok = 1;
+        std::vector<uint8_t> oks(D);
+        lamb_status st = bootstrap_allgather(h, &ok, oks.data(), 1);
+        if (st != LAMB_OK) return st;
+    }
     return LAMB_OK;
 }
 
-extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors,
-                                   const lamb_group* groups, int32_t n_groups,
-                                   const lamb_config* cfg, const uint8_t* id, lamb_t* out) {
+static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, const lamb_group* groups,
+                               int32_t n_groups, const lamb_config* cfg, const uint8_t* id,
+                               lamb_allgather_fn host_ag, void* host_ag_user, lamb_t* out) {
     if (!out || !tensors || !groups || !cfg) return fail(nullptr, LAMB_EINVAL, "null argument");
     *out = nullptr;
     if (n_groups < 1 || n_groups > LAMB_MAX_GROUPS)
@@ -333,13 +349,17 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
             return fail(nullptr, LAMB_EINVAL, "tensor " + std::to_string(i) + ": group out of range");
         if (tensors[i].reserved != 0) return fail(nullptr, LAMB_EINVAL, "reserved must be 0");
     }
-    if (cfg->world_size > 1 && !id) return fail(nullptr, LAMB_EINVAL, "unique id required for D > 1");
+    if (cfg->world_size > 1 && !id && !host_ag) return fail(nullptr, LAMB_EINVAL, "unique id required for D > 1");
+    if (cfg->world_size > 1 && host_ag && cfg->comm_mode != LAMB_COMM_FUSED)
+        return fail(nullptr, LAMB_EINVAL, "the host all-gather bootstrap needs LAMB_COMM_FUSED (no NCCL communicator)");
     if (cfg->world_size > 1 && cfg->comm_mode != LAMB_COMM_NCCL && cfg->comm_mode != LAMB_COMM_FUSED)
         return fail(nullptr, LAMB_EUNSUPPORTED, "comm_mode not supported in ABI v1");
     if (!(cfg->grad_scale >= 0.f)) return fail(nullptr, LAMB_EINVAL, "grad_scale must be >= 0");
 
     auto* h = new lamb_ctx();
     h->cfg = *cfg;
+    h->host_ag = host_ag;
+    h->host_ag_user = host_ag_user;
     h->diag_local_grads = getenv("LAMB_DIAG_LOCAL_GRADS") != nullptr;
     {
         // failure detection: bound on every cross-GPU wait (a missing peer must not hang the GPU)
@@ -446,6 +466,24 @@ extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors
     return LAMB_OK;
 #undef STEP
 #undef CUDA_STEP
+}
+
+extern "C" lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors, const lamb_group* groups,
+                                   int32_t n_groups, const lamb_config* cfg, const uint8_t* id, lamb_t* out) {
+    return create_impl(tensors, n_tensors, groups, n_groups, cfg, id, nullptr, nullptr, out);
+}
+
+extern "C" lamb_status lamb_create_with_allgather(const lamb_tensor* tensors, int64_t n_tensors,
+                                                  const lamb_group* groups, int32_t n_groups,
+                                                  const lamb_config* cfg, lamb_allgather_fn allgather,
+                                                  void* user, lamb_t* out) {
+    if (!allgather) return fail(nullptr, LAMB_EINVAL, "null all-gather callback");
+    lamb_status st = create_impl(tensors, n_tensors, groups, n_groups, cfg, nullptr, allgather, user, out);
+    if (st == LAMB_OK) {
+        (*out)->host_ag = nullptr;   // only valid during the call
+        (*out)->host_ag_user = nullptr;
+    }
+    return st;
 }
 
 extern "C" void lamb_destroy(lamb_t h) { free_ctx(h); }

@@ -84,6 +84,9 @@ _SIGS = {
     "lamb_get_unique_id": (_st, [ctypes.c_char_p]),
     "lamb_create": (_st, [ctypes.POINTER(lamb_tensor), ctypes.c_int64, ctypes.POINTER(lamb_group),
                           ctypes.c_int32, ctypes.POINTER(lamb_config), ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "lamb_create_with_allgather": (_st, [ctypes.POINTER(lamb_tensor), ctypes.c_int64, ctypes.POINTER(lamb_group),
+                                         ctypes.c_int32, ctypes.POINTER(lamb_config), _vp, _vp,
+                                         ctypes.POINTER(_vp)]),
     "lamb_step": (_st, [_vp, _vp, ctypes.c_int64, _vp]),
     "lamb_step_host": (_st, [_vp, _vp, _vp, ctypes.c_int64, _vp]),
     "lamb_step_bucket": (_st, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _vp]),
@@ -210,7 +213,7 @@ class Lamb:
     def __init__(self, tensors: Sequence[tuple], groups: Sequence, world_size: int = 1, rank: int = 0,
                  device: int = 0, comm_mode: int = LAMB_COMM_FUSED, bucket_cap: int = 0,
                  grad_scale: float = 0.0, timing: bool = False, unique_id: Optional[bytes] = None,
-                 pg=None, graph: bool = False):
+                 pg=None, graph: bool = False, bootstrap: str = "nccl"):
         import torch
         self.torch = torch
         self.device = device
@@ -227,13 +230,23 @@ class Lamb:
             garr[k].adapt, garr[k].bias_correction = int(get("adapt")), int(get("bias_correction"))
         cfg = lamb_config(world_size, rank, device, comm_mode, bucket_cap, grad_scale,
                           (LAMB_FLAG_TIMING if timing else 0) | (LAMB_FLAG_GRAPH if graph else 0))
-        if world_size > 1 and unique_id is None:
-            if pg is None:
-                raise ValueError("world_size > 1 needs unique_id or a process group")
-            unique_id = broadcast_unique_id(pg, rank, device)
         self.h = _vp()
-        check(lamb_create(self._tensors, len(numels), garr, len(groups), ctypes.byref(cfg),
-                          unique_id, ctypes.byref(self.h)))
+        if world_size > 1 and bootstrap == "host":
+            # FUSED without an NCCL communicator: IPC handles exchanged over the caller's group
+            if pg is None:
+                raise ValueError("bootstrap='host' needs a process group")
+            ag = _pg_allgather(pg)
+            check(lamb_create_with_allgather(self._tensors, len(numels), garr, len(groups), ctypes.byref(cfg),
+                                             ctypes.cast(ag, _vp), None, ctypes.byref(self.h)))
+        else:
+            if bootstrap != "nccl":
+                raise ValueError("bootstrap must be 'nccl' or 'host'")
+            if world_size > 1 and unique_id is None:
+                if pg is None:
+                    raise ValueError("world_size > 1 needs unique_id or a process group")
+                unique_id = broadcast_unique_id(pg, rank, device)
+            check(lamb_create(self._tensors, len(numels), garr, len(groups), ctypes.byref(cfg),
+                              unique_id, ctypes.byref(self.h)))
         v = lamb_plan_view()
         check(lamb_query_plan(self.h, ctypes.byref(v)), self.h)
         self.plan = PlanView(v)
@@ -371,6 +384,28 @@ class Lamb:
             self.close()
         except Exception:
             pass
+
+
+_ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+
+
+def _pg_allgather(pg):
+    """lamb_allgather_fn over a torch.distributed group (bootstrap bytes only: IPC handles,
+    the table hash).  The returned ctypes object must outlive the create call."""
+    import torch.distributed as dist
+
+    def fn(send, recv, nbytes, _user):
+        try:
+            out = [None] * dist.get_world_size(pg)
+            dist.all_gather_object(out, ctypes.string_at(send, nbytes), group=pg)
+            for j, b in enumerate(out):
+                if len(b) != nbytes:
+                    return 1
+                ctypes.memmove(recv + j * nbytes, b, nbytes)
+            return 0
+        except Exception:
+            return 1
+    return _ALLGATHER_FN(fn)
 
 
 def broadcast_unique_id(pg, rank: int, device: int) -> bytes:

@@ -24,9 +24,18 @@ import workloads as W  # noqa: E402
 from gpu_common import compare_state, spec_of  # noqa: E402
 
 
+# "nccl": one rank per GPU, NCCL bootstrap.  "host" (--oversub): D ranks over fewer GPUs
+# (device = rank % GPUs), gloo process group, lamb_create_with_allgather (no NCCL communicator).
+BOOT = "nccl"
+
+
+def _dev():
+    return torch.device("cpu") if BOOT == "host" else torch.device("cuda")
+
+
 def gather_full_w(L, world):
     """All ranks' fp32 shards -> full flat fp32 (host), via the plan's slices."""
-    w = torch.from_numpy(L.get_state(2)).cuda()
+    w = torch.from_numpy(L.get_state(2)).to(_dev())
     allw = [torch.empty_like(w) for _ in range(world)]
     dist.all_gather(allw, w)
     allw = [a.cpu().numpy() for a in allw]
@@ -43,7 +52,8 @@ def gather_full_w(L, world):
 def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, check_all_params=True):
     from paper_2402_15627_b200 import lamb
     L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
-                  device=local, comm_mode=mode, bucket_cap=cap if cap else wl.cap, pg=dist.group.WORLD)
+                  device=local, comm_mode=mode, bucket_cap=cap if cap else wl.cap, pg=dist.group.WORLD,
+                  bootstrap=BOOT)
     spec = spec_of(wl)
     L.synth_init(spec, wl.seed)
     for t in range(1, steps + 1):
@@ -65,7 +75,7 @@ def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, chec
     # identical on every rank: sampled windows (same positions everywhere) compared across ranks
     g = torch.Generator().manual_seed(7)
     starts = torch.randint(0, max(1, p.numel() - 4096), (64,), generator=g).tolist()
-    win = torch.cat([p[s0:s0 + 4096] for s0 in starts] + [p[-4096:]]).long()
+    win = torch.cat([p[s0:s0 + 4096] for s0 in starts] + [p[-4096:]]).long().to(_dev())
     hs = [torch.empty_like(win) for _ in range(world)]
     dist.all_gather(hs, win)
     assert all(torch.equal(x, hs[0]) for x in hs), f"{name}: param buffers differ across ranks"
@@ -194,7 +204,8 @@ def ckpt_case(world, rank, local, mode):
     spec = spec_of(wl)
     path = f"/tmp/lamb_ckpt_D{world}_{mode}.bin"
     mk = lambda D, r, cap, pg: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=D,
-                                         rank=r, device=local, comm_mode=mode, bucket_cap=cap, pg=pg)
+                                         rank=r, device=local, comm_mode=mode, bucket_cap=cap, pg=pg,
+                                         bootstrap=BOOT if D > 1 else "nccl")
     A = mk(world, rank, 8192, dist.group.WORLD)
     A.synth_init(spec, wl.seed)
     for t in (1, 2):
@@ -383,14 +394,36 @@ def main():
     ap.add_argument("--full", action="store_true",
                     help="only the full-size BASELINE configs: 530B+stress (all stress tensors and "
                          "LayerNorm tensors checked) and 13B (sampled), in the bench launch config")
+    ap.add_argument("--oversub", action="store_true",
+                    help="D ranks on fewer GPUs (rank %% GPUs), host bootstrap, gloo: the D-rank FUSED "
+                         "kernels and protocol (e.g. D = 8) on a smaller box")
     a = ap.parse_args()
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
     local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2402_15627_b200 import lamb
     mode = lamb.LAMB_COMM_FUSED if a.mode == "fused" else lamb.LAMB_COMM_NCCL
+    if a.oversub:
+        global BOOT
+        BOOT = "host"
+        local = rank % torch.cuda.device_count()
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+        run_case("toy", W.toy(), world, rank, local, mode, 1)
+        run_case("toy10", W.toy(), world, rank, local, mode, 10)
+        rng = np.random.default_rng(321)
+        tensors = W.random_table(rng, 60, max_numel=4000, p_big=0.15, big=50_000)
+        run_case("ragged", W.Workload("ragged", 50, tensors, W.default_groups(lr=2.0 ** -7)), world, rank,
+                 local, mode, 3, cap=8192)
+        stress = W.stress_tensors(0, 3000)
+        run_case("stress", W.Workload("stress", 51, stress, W.default_groups()), world, rank, local, mode, 2,
+                 cap=100_000)
+        ckpt_case(world, rank, local, mode)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     if a.full:
         wl = W.slice_530b_stress()

@@ -49,6 +49,28 @@ def _run(fn_name, world=2):
 
 
 # ------------------------------------------------------------------ rank bodies
+def body_host_allgather(rank, world):
+    """The bootstrap callback lamb_create_with_allgather calls (IPC handles, table hash):
+    rank j's bytes land at offset j * nbytes on every rank; a size mismatch reports failure."""
+    import ctypes
+    from paper_2402_15627_b200 import lamb
+    fn = lamb._pg_allgather(dist.group.WORLD)
+    nb = 192   # three cudaIpcMemHandle_t
+    send = (ctypes.c_uint8 * nb)(*[(rank * 31 + i) % 256 for i in range(nb)])
+    recv = (ctypes.c_uint8 * (nb * world))()
+    cfn = ctypes.cast(fn, ctypes.c_void_p)
+    call = lamb._ALLGATHER_FN(cfn.value)
+    assert call(ctypes.addressof(send), ctypes.addressof(recv), nb, None) == 0
+    got = bytes(recv)
+    for j in range(world):
+        assert got[j * nb:(j + 1) * nb] == bytes((j * 31 + i) % 256 for i in range(nb))
+    # ranks passing different sizes: every rank must see the failure, none may hang
+    nb2 = 8 + rank
+    send2 = (ctypes.c_uint8 * nb2)()
+    recv2 = (ctypes.c_uint8 * (nb2 * world))()
+    assert call(ctypes.addressof(send2), ctypes.addressof(recv2), nb2, None) == 1
+
+
 def body_unique_id(rank, world):
     from paper_2402_15627_b200 import lamb
     uid = lamb.broadcast_unique_id(dist.group.WORLD, rank, 0)
@@ -133,3 +155,7 @@ def test_plans_agree_across_ranks_gloo():
 
 def test_straddler_exchange_protocol_gloo():
     _run("body_straddler_exchange")
+
+
+def test_host_allgather_bootstrap():
+    _run("body_host_allgather")

@@ -9,8 +9,8 @@ import pytest
 torch = pytest.importorskip("torch")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
-pytestmark = [pytest.mark.gpu, pytest.mark.multigpu,
-              pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")]
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+needs2 = pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 
 
 def _torchrun(n, *args, timeout=900):
@@ -23,6 +23,7 @@ def _torchrun(n, *args, timeout=900):
     assert r.returncode == 0
 
 
+@needs2
 @pytest.mark.parametrize("mode", ["fused", "nccl"])
 def test_parity_2gpu(mode):
     _torchrun(2, "--mode", mode)
@@ -51,3 +52,11 @@ def test_full_size_530b_stress_13b_175b_4gpu():
     every stress / LayerNorm tensor of the 530B slice, sampled 13B tensors, and every vector
     plus one 603M-element matrix of the 175B slice against the oracle."""
     _torchrun(4, "--mode", "fused", "--full", timeout=1800)
+
+
+@pytest.mark.skipif(NGPU < 1, reason="needs a GPU")
+def test_parity_8ranks_oversubscribed():
+    """D = 8 FUSED on whatever GPUs the box has (ranks share devices, time-sliced): the NS = ND = 8
+    kernels, the 8-rank barrier/straddler protocol and the FUSED checkpoint reload, bootstrapped
+    without NCCL through lamb_create_with_allgather over a gloo group."""
+    _torchrun(8, "--mode", "fused", "--oversub", timeout=1200)
