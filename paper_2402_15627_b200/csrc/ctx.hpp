@@ -37,6 +37,13 @@ struct lamb_ctx {
     float *w = nullptr, *m = nullptr, *v = nullptr;   // shard
     Item* items = nullptr;
     int64_t n_items = 0;
+    // FUSED whole-table pass B order: [0, n_items_b_plain) non-straddler items, then straddler
+    // items (null when this rank touches no straddler)
+    Item* items_b = nullptr;
+    int64_t n_items_b_plain = 0;
+    cudaStream_t x_stream = nullptr;   // FUSED: straddler exchange concurrent with pass B
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool no_strad_hide = false;        // LAMB_NO_STRAD_HIDE (A/B timing)
     std::vector<int64_t> bucket_item_begin;   // [B+1] items of bucket b: [b], [b+1)
     std::vector<int64_t> bucket_seg_begin;    // [B+1] this rank's segments of bucket b
     std::vector<int64_t> bucket_strad_begin;  // [B+1] this rank's local straddler slots of bucket b

@@ -138,7 +138,7 @@ static void free_ctx(lamb_ctx* h) {
         if (h->peer_param[j] && h->peer_param[j] != h->param) cudaIpcCloseMemHandle(h->peer_param[j]);
         if (h->peer_sync[j] && h->peer_sync[j] != h->sync) cudaIpcCloseMemHandle(h->peer_sync[j]);
     }
-    void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->partials, h->segs, h->scale,
+    void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->items_b, h->partials, h->segs, h->scale,
                     h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
                     h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_clip_blocks, h->d_groups, h->d_shard_pad, h->d_flat_pad, h->d_check, h->d_tensor_off, h->d_numel,
                     h->d_shard_base, h->d_bucket_base, h->d_bucket_slice};
@@ -149,9 +149,10 @@ static void free_ctx(lamb_ctx* h) {
     for (auto* vec : {&h->ev_rs, &h->ev_b, &h->tev})
         for (cudaEvent_t e : *vec) cudaEventDestroy(e);
     for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_grad_free, h->ev_h2d, h->ev_params, h->ev_d2h,
-                          h->ev_call})
+                          h->ev_call, h->ev_fork, h->ev_join})
         if (e) cudaEventDestroy(e);
-    for (cudaStream_t st : {h->comm_stream, h->h2d_stream, h->d2h_stream, h->work_stream, h->cap_stream})
+    for (cudaStream_t st : {h->comm_stream, h->h2d_stream, h->d2h_stream, h->work_stream, h->cap_stream,
+                            h->x_stream})
         if (st) cudaStreamDestroy(st);
     if (h->comm) ncclCommDestroy(h->comm);
     delete h;
@@ -219,6 +220,19 @@ static lamb_status build_tables(lamb_ctx* h) {
     h->n_items = (int64_t)items.size();
     h->n_local_strad = (int32_t)ls_slot.size();
     CUDA_TRY(h, upload(&h->items, items));
+    if (p.world > 1 && h->n_local_strad > 0) {
+        // pass B order for the whole-table FUSED step: items of non-straddler tensors first (their
+        // trust ratios are final after the local finalize), straddler items last (they wait for the
+        // cross-rank exchange, which runs on a side stream meanwhile)
+        std::vector<Item> ib;
+        ib.reserve(items.size());
+        for (const Item& it : items)
+            if (strad_slot_of[it.tensor] < 0) ib.push_back(it);
+        h->n_items_b_plain = (int64_t)ib.size();
+        for (const Item& it : items)
+            if (strad_slot_of[it.tensor] >= 0) ib.push_back(it);
+        CUDA_TRY(h, upload(&h->items_b, ib));
+    }
     CUDA_TRY(h, upload(&h->segs, segs));
     CUDA_TRY(h, upload(&h->strad_slots, ls_slot));
     CUDA_TRY(h, upload(&h->strad_tensor, ls_tensor));
@@ -448,6 +462,12 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
     }
     if (D > 1) {
         STEP(setup_comm(h, id));
+        if (cfg->comm_mode == LAMB_COMM_FUSED) {
+            CUDA_STEP(cudaStreamCreateWithFlags(&h->x_stream, cudaStreamNonBlocking));
+            CUDA_STEP(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+            CUDA_STEP(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+            h->no_strad_hide = getenv("LAMB_NO_STRAD_HIDE") != nullptr;
+        }
         if (cfg->comm_mode == LAMB_COMM_NCCL) {
             CUDA_STEP(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
             CUDA_STEP(dalloc(&h->g32, (size_t)p.shard_size));
@@ -620,21 +640,48 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         for (int j = 0; j < D; ++j) fp.xrow[j] = h->xbuf(fused ? j : -1);
         LAUNCH(h, launch_finalize_segments(fp, s));
         mark(h, 3, s);
-        if (fused && strad) {
-            // straddler rows travel through peer memory: barrier, then sum in rank order
-            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
-            if (fp.n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
-        }
-        mark(h, 4, s);
-        if (h->pre_b_event) {
-            // lamb_step_host: the previous step's download of the param buffer(s) must finish
-            // before pass B rewrites them — on every rank, since pass B stores into peers
-            CUDA_TRY(h, cudaStreamWaitEvent(s, h->pre_b_event, 0));
-            if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
-        }
         const bool push = fused && !defer_ag;
         for (int j = 0; j < D; ++j) sp.pdst[j] = push ? h->peer_param[j] : h->param;
-        LAUNCH(h, launch_pass_b(sp, push ? D : 1, grid_b, s));
+        // Straddler exchange hidden behind pass B (whole-table FUSED step): pass B streams the
+        // non-straddler items while a side stream runs barrier + straddler finalize; the
+        // straddler items follow once their ratios are final.  Every barrier stays in one
+        // global order on every rank (the pre-B barrier precedes the fork).
+        const bool hide = fused && strad && whole && !defer_ag && h->items_b && !h->no_strad_hide;
+        if (hide) {
+            if (h->pre_b_event) {
+                CUDA_TRY(h, cudaStreamWaitEvent(s, h->pre_b_event, 0));
+                LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
+            }
+            CUDA_TRY(h, cudaEventRecord(h->ev_fork, s));
+            CUDA_TRY(h, cudaStreamWaitEvent(h->x_stream, h->ev_fork, 0));
+            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, h->x_stream, h->barrier_timeout_ns));
+            if (fp.n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, h->x_stream));
+            CUDA_TRY(h, cudaEventRecord(h->ev_join, h->x_stream));
+            mark(h, 4, s);
+            StepParams sb = sp;
+            sb.items = h->items_b;
+            sb.item_begin = 0;
+            sb.item_end = h->n_items_b_plain;
+            LAUNCH(h, launch_pass_b(sb, D, grid_b, s));
+            CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_join, 0));
+            sb.item_begin = h->n_items_b_plain;
+            sb.item_end = h->n_items;
+            LAUNCH(h, launch_pass_b(sb, D, grid_b, s));
+        } else {
+            if (fused && strad) {
+                // straddler rows travel through peer memory: barrier, then sum in rank order
+                LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
+                if (fp.n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(fp, s));
+            }
+            mark(h, 4, s);
+            if (h->pre_b_event) {
+                // lamb_step_host: the previous step's download of the param buffer(s) must finish
+                // before pass B rewrites them — on every rank, since pass B stores into peers
+                CUDA_TRY(h, cudaStreamWaitEvent(s, h->pre_b_event, 0));
+                if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
+            }
+            LAUNCH(h, launch_pass_b(sp, push ? D : 1, grid_b, s));
+        }
         mark(h, 5, s);
         if (fused) {
             // params complete everywhere, and every rank finished reading this rank's grads

@@ -271,6 +271,38 @@ def graph_case(world, rank, local, mode):
         print(f"[ok] CUDA-graph step D={world} == eager (bitwise)", flush=True)
 
 
+def hide_case(world, rank, local, mode):
+    """FUSED: the straddler exchange hidden behind pass B (side stream, straddler items last) ==
+    the serial order (LAMB_NO_STRAD_HIDE), bitwise — w, m, v and every param buffer."""
+    from paper_2402_15627_b200 import lamb
+    if mode != lamb.LAMB_COMM_FUSED:
+        return
+    stress = W.stress_tensors(0, 2000)
+    wl = W.Workload("hide", 77, stress, W.default_groups())
+    spec = spec_of(wl)
+    out = []
+    for env in (None, "1"):
+        if env:
+            os.environ["LAMB_NO_STRAD_HIDE"] = env
+        L = lamb.Lamb([(t.numel, t.group) for t in stress], wl.groups, world_size=world, rank=rank,
+                      device=local, comm_mode=mode, bucket_cap=60_000, pg=dist.group.WORLD, bootstrap=BOOT)
+        os.environ.pop("LAMB_NO_STRAD_HIDE", None)
+        assert len(L.plan.straddlers) > 0
+        L.synth_init(spec, wl.seed)
+        for t in (1, 2, 3):
+            L.synth_grads(spec, wl.seed, rank + 1, t)
+            L.step(t)
+        torch.cuda.synchronize()
+        out.append([L.get_state(k).view(np.uint32).copy() for k in (2, 3, 4)] +
+                   [L.param_buffer().view(torch.int16).cpu().numpy().copy()])
+        L.close()
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] straddler exchange hidden behind pass B D={world} == serial (bitwise)", flush=True)
+
+
 def h10_case(world, rank, local, mode):
     """Pin H10 on the GPU: the fp32 reduced gradient (NCCL reduce-scatter of the upcast grads,
     or the fused peer-load sum) equals the exact D-rank sum bit-for-bit (the generator's
@@ -419,6 +451,7 @@ def main():
         run_case("stress", W.Workload("stress", 51, stress, W.default_groups()), world, rank, local, mode, 2,
                  cap=100_000)
         ckpt_case(world, rank, local, mode)
+        hide_case(world, rank, local, mode)
         dist.barrier()
         dist.destroy_process_group()
         return
@@ -461,6 +494,7 @@ def main():
     host_case(world, rank, local, mode)
     graph_case(world, rank, local, mode)
     h10_case(world, rank, local, mode)
+    hide_case(world, rank, local, mode)
     torch_case(world, rank, local, mode)
     os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"
     failure_case(world, rank, local, mode)

@@ -81,6 +81,67 @@ float run(int D, size_t bpp, std::vector<char*>& remote, std::vector<char*>& loc
     return (float)(bpp * (D - 1)) / (best * 1e-3f) / 1e9f;
 }
 
+// Copy-engine all-to-all: every GPU issues one cudaMemcpyPeerAsync per peer, each on its own
+// stream (PUSH: from the GPU's local buffer into the peer; pull: from the peer into local).
+float run_ce(int D, size_t bpp, std::vector<char*>& remote, std::vector<char*>& local, bool push, int split) {
+    std::vector<cudaEvent_t> e0(D), e1(D);
+    std::vector<std::vector<cudaStream_t>> st(D);
+    for (int g = 0; g < D; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaEventCreate(&e0[g]));
+        CK(cudaEventCreate(&e1[g]));
+        st[g].resize((D - 1) * split);
+        for (auto& x : st[g]) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    }
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaDeviceSynchronize());
+        }
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaEventRecord(e0[g], 0));
+            int k = 0;
+            for (int j = 0; j < D; ++j) {
+                if (j == g) continue;
+                for (int q = 0; q < split; ++q, ++k) {
+                    const size_t lo = bpp * q / split, n = bpp * (q + 1) / split - lo;
+                    CK(cudaStreamWaitEvent(st[g][k], e0[g], 0));
+                    if (push)
+                        CK(cudaMemcpyPeerAsync(remote[j] + (size_t)g * bpp + lo, j, local[g] + (size_t)j * bpp + lo,
+                                               g, n, st[g][k]));
+                    else
+                        CK(cudaMemcpyPeerAsync(local[g] + (size_t)j * bpp + lo, g, remote[j] + (size_t)g * bpp + lo,
+                                               j, n, st[g][k]));
+                }
+            }
+            for (auto& x : st[g]) {
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(ev, x));
+                CK(cudaStreamWaitEvent(0, ev, 0));
+                CK(cudaEventDestroy(ev));
+            }
+            CK(cudaEventRecord(e1[g], 0));
+        }
+        float worst = 0;
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaEventSynchronize(e1[g]));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0[g], e1[g]));
+            worst = ms > worst ? ms : worst;
+        }
+        best = worst < best ? worst : best;
+    }
+    for (int g = 0; g < D; ++g) {
+        CK(cudaSetDevice(g));
+        for (auto& x : st[g]) CK(cudaStreamDestroy(x));
+    }
+    return (float)(bpp * (D - 1)) / (best * 1e-3f) / 1e9f;
+}
+
 int main(int argc, char** argv) {
     const int D = argc > 1 ? atoi(argv[1]) : 2;
     const size_t mib = argc > 2 ? (size_t)atoll(argv[2]) : 512;
@@ -110,6 +171,10 @@ int main(int argc, char** argv) {
         printf(", \"pull16_x%d\": %.1f", mult, run<uint4, false>(D, bpp, remote, local, grid));
         printf(", \"push8_x%d\": %.1f", mult, run<uint2, true>(D, bpp, remote, local, grid));
         printf(", \"push16_x%d\": %.1f", mult, run<uint4, true>(D, bpp, remote, local, grid));
+    }
+    for (int split : {1, 4}) {
+        printf(", \"ce_push_s%d\": %.1f", split, run_ce(D, bpp, remote, local, true, split));
+        printf(", \"ce_pull_s%d\": %.1f", split, run_ce(D, bpp, remote, local, false, split));
     }
     printf("}\n");
     return 0;
