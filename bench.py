@@ -127,7 +127,7 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.h = nvml_handle(pynvml, device)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
         except Exception as e:  # pragma: no cover
@@ -166,6 +166,34 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ our arm
+def nvml_handle(pynvml, device: int):
+    """NVML handle of CUDA device `device` (matched by UUID: CUDA and NVML orders may differ)."""
+    import torch
+    try:
+        return pynvml.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(device).uuid))
+    except Exception:
+        return pynvml.nvmlDeviceGetHandleByIndex(device)
+
+
+def bind_numa_local(device: int):
+    """Pin this rank to the CPUs NVML reports as local to its GPU, so the pinned host buffers of
+    the e2e leg are first-touched on the GPU's NUMA node (one rank per GPU share the host)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = nvml_handle(pynvml, device)
+        n = (os.cpu_count() + 63) // 64
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, n)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        pass
+    return None
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -239,6 +267,7 @@ def main():
     # ---------------- e2e: host buffers through lamb_step_host (H2D grads + D2H params in region)
     e2e = None
     if not args.no_e2e:
+        numa_cpus = bind_numa_local(local) if world > 1 else None
         flat = L.plan.flat_size
         hg = torch.empty(flat, dtype=torch.bfloat16, pin_memory=True)
         hg.copy_(L.grad_buffer())
@@ -259,7 +288,8 @@ def main():
             ms_e2e = float(tt[0])
         e2e = {"value": wl.n_params / (ms_e2e / 1e3), "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": 2 * flat * world, "d2h_bytes_per_step": 2 * flat * world,
-               "steps": Ke, "api": "lamb_step_host (pinned host grads in, params out)"}
+               "steps": Ke, "api": "lamb_step_host (pinned host grads in, params out)",
+               "numa_local_cpus": numa_cpus}
 
     if rank != 0:
         L.close()

@@ -79,6 +79,12 @@ struct lamb_ctx {
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr, work_stream = nullptr;
     cudaEvent_t ev_h2d = nullptr, ev_params = nullptr, ev_d2h = nullptr, ev_call = nullptr;
     cudaEvent_t pre_b_event = nullptr;   // step_impl waits on it before pass B (lamb_step_host)
+    // lamb_step_host per-bucket pipeline: grads of b landed / consumed, params of b ready /
+    // downloaded (one event each per bucket)
+    std::vector<cudaEvent_t> ev_hb, ev_gf, ev_pb, ev_db;
+    cudaEvent_t gf_override = nullptr;   // step_impl records "grads consumed" here if set
+    bool host_whole = false;             // LAMB_HOST_WHOLE: whole-step pipeline (A/B timing)
+    cudaEvent_t grad_free_event() const { return gf_override ? gf_override : ev_grad_free; }
     int grid_a = 0, grid_b = 0;
     int max_ctas = 0;   // SM budget of the streaming passes (0 = one full wave)
     bool diag_local_grads = false;   // LAMB_DIAG_LOCAL_GRADS: timing diagnostic, wrong results

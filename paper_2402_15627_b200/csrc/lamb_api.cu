@@ -146,7 +146,7 @@ static void free_ctx(lamb_ctx* h) {
         if (p) cudaFree(p);
     if (h->err_flag_host) cudaFreeHost(h->err_flag_host);
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-    for (auto* vec : {&h->ev_rs, &h->ev_b, &h->tev})
+    for (auto* vec : {&h->ev_rs, &h->ev_b, &h->tev, &h->ev_hb, &h->ev_gf, &h->ev_pb, &h->ev_db})
         for (cudaEvent_t e : *vec) cudaEventDestroy(e);
     for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_grad_free, h->ev_h2d, h->ev_params, h->ev_d2h,
                           h->ev_call, h->ev_fork, h->ev_join})
@@ -466,7 +466,8 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
             CUDA_STEP(cudaStreamCreateWithFlags(&h->x_stream, cudaStreamNonBlocking));
             CUDA_STEP(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
             CUDA_STEP(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
-            h->no_strad_hide = getenv("LAMB_NO_STRAD_HIDE") != nullptr;
+            const char* e = getenv("LAMB_NO_STRAD_HIDE");
+            h->no_strad_hide = e && *e && *e != '0';
         }
         if (cfg->comm_mode == LAMB_COMM_NCCL) {
             CUDA_STEP(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
@@ -635,7 +636,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         } else {
             LAUNCH(h, launch_pass_a(sp, D, false, grid_a, s));
         }
-        if (!fused) CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));   // D = 1: grads consumed
+        if (!fused) CUDA_TRY(h, cudaEventRecord(h->grad_free_event(), s));   // D = 1: grads consumed
         mark(h, 2, s);
         for (int j = 0; j < D; ++j) fp.xrow[j] = h->xbuf(fused ? j : -1);
         LAUNCH(h, launch_finalize_segments(fp, s));
@@ -686,7 +687,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         if (fused) {
             // params complete everywhere, and every rank finished reading this rank's grads
             LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
-            CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));
+            CUDA_TRY(h, cudaEventRecord(h->grad_free_event(), s));
         }
         mark(h, 6, s);
         return LAMB_OK;
@@ -751,7 +752,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     }
     CUDA_TRY(h, cudaEventRecord(h->ev_done, h->comm_stream));
     CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_done, 0));
-    CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));
+    CUDA_TRY(h, cudaEventRecord(h->grad_free_event(), s));
     mark(h, 5, s);
     mark(h, 6, s);
     return LAMB_OK;
@@ -874,19 +875,28 @@ extern "C" lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream
 
 extern "C" lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint16_t* host_params,
                                       int64_t step, void* stream) {
-    // Three-stage pipeline across consecutive calls, on internal streams:
-    //   copy-in  : H2D of this step's grads, as soon as the previous step released the grad
-    //              buffer (ev_grad_free) — concurrent with the previous step's download;
-    //   work     : the LAMB step; only pass B waits for the previous download (it rewrites the
-    //              param buffers), so pass A overlaps it too;
-    //   copy-out : D2H of the updated params.
-    // `stream` gets a dependency on the download: it completes once host_params holds the
-    // params.  The first call also orders the pipeline after the work already on `stream`.
+    // Pipeline on internal streams, per bucket and across consecutive calls (§3.2
+    // overlap "on a model chunk basis"; here the chunks hide the LAMB work and the
+    // two copy directions behind each other on the host link):
+    //   copy-in  (h2d)  : grads of bucket b, as soon as the previous step's pass A of bucket b
+    //                     released that part of the grad buffer;
+    //   work            : the LAMB update of bucket b (lamb_step_bucket: pass A, norms, ratios,
+    //                     pass B) once its grads landed; pass B also waits for the previous
+    //                     step's download of bucket b (it rewrites those params);
+    //   copy-out (d2h)  : params of bucket b as soon as its pass B finished.
+    // Every tensor lives in one bucket, so the per-bucket update is the exact LAMB step
+    // (bit-identical to lamb_step: tests).  With the pre-step (global clip / loss scale) the
+    // whole table is one unit: whole-step pipeline.  `stream` gets a dependency on the last
+    // download; the first call also orders the pipeline after the work already on `stream`.
     if (!h || !host_grads || !host_params) return fail(h, LAMB_EINVAL, "null argument");
     if (step < 1) return fail(h, LAMB_EINVAL, "step must be >= 1");
     if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step_host before lamb_set_master / lamb_synth_init");
+    lamb_status st = check_async(h);
+    if (st != LAMB_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaSetDevice(h->device);
+    const Plan& p = h->plan;
+    const int64_t B = p.n_buckets();
     if (!h->h2d_stream) {
         CUDA_TRY(h, cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
         CUDA_TRY(h, cudaStreamCreateWithFlags(&h->d2h_stream, cudaStreamNonBlocking));
@@ -895,22 +905,71 @@ extern "C" lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint
         CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_params, cudaEventDisableTiming));
         CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_d2h, cudaEventDisableTiming));
         CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_call, cudaEventDisableTiming));
+        for (auto* vec : {&h->ev_hb, &h->ev_gf, &h->ev_pb, &h->ev_db}) {
+            vec->resize(B);
+            for (auto& e : *vec) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        h->host_whole = getenv("LAMB_HOST_WHOLE") && *getenv("LAMB_HOST_WHOLE") && *getenv("LAMB_HOST_WHOLE") != '0';
         CUDA_TRY(h, cudaEventRecord(h->ev_call, s));
         CUDA_TRY(h, cudaStreamWaitEvent(h->work_stream, h->ev_call, 0));
         CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_call, 0));
     }
-    const size_t bytes = (size_t)h->plan.flat_size * 2;
+    // an earlier lamb_step may still read the grad buffer
     CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_grad_free, 0));
-    CUDA_TRY(h, cudaMemcpyAsync(h->grad, host_grads, bytes, cudaMemcpyHostToDevice, h->h2d_stream));
-    CUDA_TRY(h, cudaEventRecord(h->ev_h2d, h->h2d_stream));
-    CUDA_TRY(h, cudaStreamWaitEvent(h->work_stream, h->ev_h2d, 0));
-    h->pre_b_event = h->ev_d2h;   // previous download (a never-recorded event is a no-op)
-    lamb_status st = lamb_step(h, nullptr, step, h->work_stream);
-    h->pre_b_event = nullptr;
+    if (h->host_whole || h->prestep()) {
+        const size_t bytes = (size_t)p.flat_size * 2;
+        // the per-bucket pipeline of the previous call may still use the buffers
+        for (int64_t b = 0; b < B; ++b) CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_gf[b], 0));
+        CUDA_TRY(h, cudaMemcpyAsync(h->grad, host_grads, bytes, cudaMemcpyHostToDevice, h->h2d_stream));
+        CUDA_TRY(h, cudaEventRecord(h->ev_h2d, h->h2d_stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->work_stream, h->ev_h2d, 0));
+        for (int64_t b = 0; b < B; ++b) CUDA_TRY(h, cudaStreamWaitEvent(h->work_stream, h->ev_db[b], 0));
+        h->pre_b_event = h->ev_d2h;   // previous download (a never-recorded event is a no-op)
+        st = lamb_step(h, nullptr, step, h->work_stream);
+        h->pre_b_event = nullptr;
+        if (st != LAMB_OK) return st;
+        CUDA_TRY(h, cudaEventRecord(h->ev_params, h->work_stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->d2h_stream, h->ev_params, 0));
+        CUDA_TRY(h, cudaMemcpyAsync(host_params, h->param, bytes, cudaMemcpyDeviceToHost, h->d2h_stream));
+        CUDA_TRY(h, cudaEventRecord(h->ev_d2h, h->d2h_stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_d2h, 0));
+        return LAMB_OK;
+    }
+    // a whole-step call before may still download / own the param buffer
+    CUDA_TRY(h, cudaStreamWaitEvent(h->work_stream, h->ev_d2h, 0));
+    for (int64_t b = 0; b < B; ++b) {
+        const int64_t base = p.buckets[4 * b], S = p.buckets[4 * b + 1];
+        CUDA_TRY(h, cudaStreamWaitEvent(h->h2d_stream, h->ev_gf[b], 0));
+        CUDA_TRY(h, cudaMemcpyAsync(h->grad + base, host_grads + base, (size_t)S * 2, cudaMemcpyHostToDevice,
+                                    h->h2d_stream));
+        CUDA_TRY(h, cudaEventRecord(h->ev_hb[b], h->h2d_stream));
+    }
+    const int32_t t_max = h->t_max;
+    h->t_max = 0;   // per-bucket calls are not phase-timed
+    st = prologue(h, step, h->work_stream);
+    for (int64_t b = 0; b < B && st == LAMB_OK; ++b) {
+        const int64_t base = p.buckets[4 * b], S = p.buckets[4 * b + 1];
+        cudaError_t ce = cudaStreamWaitEvent(h->work_stream, h->ev_hb[b], 0);
+        if (ce != cudaSuccess) {
+            st = fail(h, LAMB_ECUDA, std::string("cudaStreamWaitEvent: ") + cudaGetErrorString(ce));
+            break;
+        }
+        h->pre_b_event = h->ev_db[b];   // previous download of this bucket
+        h->gf_override = h->ev_gf[b];   // this bucket's grads consumed
+        st = step_impl(h, nullptr, step, h->work_stream, b, b + 1, false);
+        h->pre_b_event = nullptr;
+        h->gf_override = nullptr;
+        if (st != LAMB_OK) break;
+        ce = cudaEventRecord(h->ev_pb[b], h->work_stream);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(h->d2h_stream, h->ev_pb[b], 0);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(host_params + base, h->param + base, (size_t)S * 2, cudaMemcpyDeviceToHost,
+                                 h->d2h_stream);
+        if (ce == cudaSuccess) ce = cudaEventRecord(h->ev_db[b], h->d2h_stream);
+        if (ce != cudaSuccess) st = fail(h, LAMB_ECUDA, std::string("bucket pipeline: ") + cudaGetErrorString(ce));
+    }
+    h->t_max = t_max;
     if (st != LAMB_OK) return st;
-    CUDA_TRY(h, cudaEventRecord(h->ev_params, h->work_stream));
-    CUDA_TRY(h, cudaStreamWaitEvent(h->d2h_stream, h->ev_params, 0));
-    CUDA_TRY(h, cudaMemcpyAsync(host_params, h->param, bytes, cudaMemcpyDeviceToHost, h->d2h_stream));
     CUDA_TRY(h, cudaEventRecord(h->ev_d2h, h->d2h_stream));
     CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_d2h, 0));
     return LAMB_OK;

@@ -85,7 +85,7 @@ def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, chec
     L.close()
     if rank == 0:
         print(f"[ok] {name} D={world} mode={mode} steps={steps} straddlers={n_strad} "
-              f"max rel err w={worst:.2e}", flush=True)
+              f"max rel err w (|w|>=1e-3)={worst:.2e}", flush=True)
 
 
 def clip_case(world, rank, local, mode):

@@ -195,27 +195,42 @@ def test_gpt13b_layout_1p3b_full_size_sampled(lamb):
     L.close()
 
 
-def test_step_host_pipeline_matches_device_steps(lamb):
-    """lamb_step_host over several consecutive steps (upload of step t+1 overlapping the
-    download of step t) is bit-identical to lamb_step on device-resident grads."""
-    wl = W.toy()
+@pytest.mark.parametrize("case", ["toy", "ragged-buckets", "mixed-whole"])
+def test_step_host_pipeline_matches_device_steps(lamb, case):
+    """lamb_step_host over several consecutive steps (per-bucket pipeline: uploads of step t+1
+    overlapping the LAMB work and the downloads of step t) is bit-identical to lamb_step on
+    device-resident grads.  "mixed-whole": steps with the pre-step enabled take the whole-step
+    pipeline, interleaved with per-bucket steps."""
+    if case == "toy":
+        wl, cap = W.toy(), 0
+    else:
+        rng = np.random.default_rng(29)
+        wl = W.Workload("hb", 73, W.random_table(rng, 40, max_numel=7000, p_big=0.2, big=40_000),
+                        W.default_groups(lr=2.0 ** -7))
+        cap = 10_000
     spec = spec_of(wl)
-    A = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups)
-    B = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups)
+    n = 5
+    A = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, bucket_cap=cap)
+    B = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, bucket_cap=cap)
+    if case != "toy":
+        assert A.plan.buckets.shape[0] > 4
     A.synth_init(spec, wl.seed)
     B.synth_init(spec, wl.seed)
-    hg = [torch.empty(A.plan.flat_size, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
-    hp = [torch.empty(A.plan.flat_size, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
-    for t in range(1, 5):
+    hg = [torch.empty(A.plan.flat_size, dtype=torch.bfloat16).pin_memory() for _ in range(n)]
+    hp = [torch.empty(A.plan.flat_size, dtype=torch.bfloat16).pin_memory() for _ in range(n)]
+    for t in range(1, n + 1):
         A.synth_grads(spec, wl.seed, 1, t)
         hg[t - 1].copy_(A.grad_buffer())
     torch.cuda.synchronize()
     A.grad_buffer().zero_()
-    for t in range(1, 5):
+    clip_at = {3} if case == "mixed-whole" else set()
+    for t in range(1, n + 1):
+        A.set_grad_clip(0.05 if t in clip_at else 0.0)
         A.step_host(hg[t - 1], hp[t - 1], t)        # no sync between calls
     torch.cuda.synchronize()
-    for t in range(1, 5):
+    for t in range(1, n + 1):
         B.synth_grads(spec, wl.seed, 1, t)
+        B.set_grad_clip(0.05 if t in clip_at else 0.0)
         B.step(t)
         torch.cuda.synchronize()
         assert torch.equal(hp[t - 1].view(torch.int16), B.param_buffer().cpu().view(torch.int16)), t
