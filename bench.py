@@ -267,7 +267,7 @@ def main():
     # ---------------- e2e: host buffers through lamb_step_host (H2D grads + D2H params in region)
     e2e = None
     if not args.no_e2e:
-        numa_cpus = bind_numa_local(local) if world > 1 else None
+        numa_cpus = bind_numa_local(local) if world > 1 and os.environ.get("LAMB_BENCH_NUMA", "1") != "0" else None
         flat = L.plan.flat_size
         hg = torch.empty(flat, dtype=torch.bfloat16, pin_memory=True)
         hg.copy_(L.grad_buffer())
