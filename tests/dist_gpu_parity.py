@@ -271,6 +271,34 @@ def graph_case(world, rank, local, mode):
         print(f"[ok] CUDA-graph step D={world} == eager (bitwise)", flush=True)
 
 
+def replicated_case(world, rank, local, mode):
+    """H8 on the GPU: every rank feeds the SAME gradients (REPLICATED generator stream), so the
+    DP mean is that gradient and the D-rank sharded step must match the UNSHARDED oracle run
+    at D = 1 (sharding is only an execution strategy)."""
+    from paper_2402_15627_b200 import lamb
+    rng = np.random.default_rng(404)
+    tensors = W.random_table(rng, 40, max_numel=6000, p_big=0.2, big=60_000)
+    wl = W.Workload("repl", 78, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    L = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
+                  device=local, comm_mode=mode, bucket_cap=9000, pg=dist.group.WORLD, bootstrap=BOOT)
+    L.synth_init(spec, wl.seed)
+    steps = 10
+    for t in range(1, steps + 1):
+        L.synth_grads(spec, wl.seed, oracle.rank_term(oracle.REPLICATED, rank), t)
+        L.step(t)
+    torch.cuda.synchronize()
+    orc = oracle.OracleRun(wl, world_size=1, mode=oracle.REPLICATED)
+    for t in range(1, steps + 1):
+        orc.step(t)
+    worst = compare_state(L, orc, steps, check_params=False)
+    L.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] H8 REPLICATED D={world} == unsharded oracle (D=1), 10 steps, "
+              f"max rel err w={worst:.2e}", flush=True)
+
+
 def hide_case(world, rank, local, mode):
     """FUSED: the straddler exchange hidden behind pass B (side stream, straddler items last) ==
     the serial order (LAMB_NO_STRAD_HIDE), bitwise — w, m, v and every param buffer."""
@@ -452,6 +480,7 @@ def main():
                  cap=100_000)
         ckpt_case(world, rank, local, mode)
         hide_case(world, rank, local, mode)
+        replicated_case(world, rank, local, mode)
         dist.barrier()
         dist.destroy_process_group()
         return
@@ -495,6 +524,7 @@ def main():
     graph_case(world, rank, local, mode)
     h10_case(world, rank, local, mode)
     hide_case(world, rank, local, mode)
+    replicated_case(world, rank, local, mode)
     torch_case(world, rank, local, mode)
     os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"
     failure_case(world, rank, local, mode)

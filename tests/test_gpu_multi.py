@@ -32,7 +32,7 @@ def test_parity_2gpu(mode):
 @pytest.mark.skipif(NGPU < 4, reason="needs >= 4 GPUs")
 @pytest.mark.parametrize("mode", ["fused", "nccl"])
 def test_parity_4gpu(mode):
-    _torchrun(4, "--mode", mode)
+    _torchrun(4, "--mode", mode, *(["--big"] if mode == "fused" else []))
 
 
 @pytest.mark.skipif(NGPU < 3, reason="needs >= 3 GPUs")
