@@ -562,6 +562,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     sp.item_begin = h->bucket_item_begin[b0];
     sp.item_end = h->bucket_item_begin[b1];
     sp.grad_scale = h->cfg.grad_scale;
+    sp.self_src = h->cfg.world_size > 1 ? h->cfg.rank : 0;
     sp.w = h->w;
     sp.m = h->m;
     sp.v = h->v;

@@ -477,6 +477,150 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
     }
 }
 
+// ------------------------------------------------------------ pass A, TMA with a decoupled gradient ring
+// (FUSED, NS >= 2).  Same math and reduction order as pass_a_tma_kernel, but the gradient slices
+// pulled over NVLink travel in their own GS-stage ring and are issued L = GS - SS items ahead of
+// the item's m/v/w (SS-stage ring): the remote reads, whose latency the single ring exposed at
+// D = 2 (pass A 90 % of HBM vs 99 % with local-only sources), get a deep prefetch without
+// duplicating the state ring.  OWN: this rank's local slice rides in the state ring, only the
+// NS - 1 remote slices in the deep ring.  Tunable (LAMB_TUNE tmam=2..5).
+template <int NR>
+struct TmaGradStage {
+    uint2 g[NR][kTmaItem / 4];
+};
+template <bool OWN>
+struct TmaStateStage {
+    float4 m[kTmaItem / 4], v[kTmaItem / 4], w[kTmaItem / 4];
+    uint2 g[OWN ? kTmaItem / 4 : 1];
+};
+template <int NS, int SS, bool OWN>
+__host__ __device__ constexpr int tma2_grad_stages() {
+    // fill what the state ring leaves of 227 KB (1 KB reserve for barriers / statics)
+    return (int)((227 * 1024 - 1024 - (int)sizeof(TmaStateStage<OWN>) * SS) /
+                 (int)sizeof(TmaGradStage<OWN ? NS - 1 : NS>));
+}
+
+template <int NS, int SS, bool OWN>
+__global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(const __grid_constant__ StepParams P) {
+    // lead L = GS - SS: state(i) is issued once grads(i + L) are, which needs the grad slot of
+    // item i + L - GS = i - SS consumed — the same condition the state ring itself imposes, so
+    // the state ring keeps its full depth while the grads run L items further ahead
+    constexpr int NR = OWN ? NS - 1 : NS;   // sources in the deep ring
+    constexpr int GS = tma2_grad_stages<NS, SS, OWN>(), L = GS - SS;
+    static_assert(GS >= SS, "gradient ring shallower than the state ring");
+    using Stage = TmaStateStage<OWN>;
+    extern __shared__ __align__(128) unsigned char tma2_smem[];
+    Stage* st = reinterpret_cast<Stage*>(tma2_smem);
+    TmaGradStage<NR>* gr = reinterpret_cast<TmaGradStage<NR>*>(tma2_smem + sizeof(Stage) * SS);
+    uint64_t* full = reinterpret_cast<uint64_t*>(tma2_smem + sizeof(Stage) * SS + sizeof(TmaGradStage<NR>) * GS);
+    uint64_t* empty = full + SS;
+    uint64_t* gfull = empty + SS;
+    uint64_t* gempty = gfull + GS;
+    __shared__ double red_w[kTmaConsumers / 32], red_u[kTmaConsumers / 32];
+    const int tid = threadIdx.x;
+    if (P.clip && P.clip->skip) return;
+    if (tid == 0) {
+        for (int k = 0; k < SS; ++k) {
+            mbar_init(full + k, 1);
+            mbar_init(empty + k, kTmaConsumers / 32);
+        }
+        for (int k = 0; k < GS; ++k) {
+            mbar_init(gfull + k, 1);
+            mbar_init(gempty + k, kTmaConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int self = P.self_src;
+    const int64_t first = P.item_begin + blockIdx.x, stride = gridDim.x;
+    if (tid >= kTmaConsumers) {
+        if (tid == kTmaConsumers) {
+            // step i issues grads(i) then state(i - L); consumers need both, and L <= GS - SS
+            // keeps both rings live (no deadlock)
+            int kg = 0, ks = 0;
+            uint32_t pg = 0, ps = 0;
+            int64_t si = first;   // next item whose state is issued
+            for (int64_t it = first;; it += stride) {
+                const bool more = it < P.item_end;
+                if (more) {
+                    mbar_wait(gempty + kg, pg ^ 1);
+                    const Item I = P.items[it];
+                    const uint32_t ng = (uint32_t)I.n_chunk * 8u;
+                    mbar_expect_tx(gfull + kg, NR * ng);
+#pragma unroll
+                    for (int j = 0, q = 0; j < NS; ++j) {
+                        if (OWN && j == self) continue;
+                        bulk_g2s(gr[kg].g[q++], P.gsrc[j] + I.flat_off, ng, gfull + kg);
+                    }
+                    if (++kg == GS) { kg = 0; pg ^= 1; }
+                }
+                while (si < P.item_end && (!more || si <= it - (int64_t)L * stride)) {
+                    mbar_wait(empty + ks, ps ^ 1);
+                    const Item I = P.items[si];
+                    const uint32_t nf = (uint32_t)I.n_chunk * 16u, ng = (uint32_t)I.n_chunk * 8u;
+                    mbar_expect_tx(full + ks, 3 * nf + (OWN ? ng : 0));
+                    bulk_g2s(st[ks].m, P.m + I.shard_off, nf, full + ks);
+                    bulk_g2s(st[ks].v, P.v + I.shard_off, nf, full + ks);
+                    bulk_g2s(st[ks].w, P.w + I.shard_off, nf, full + ks);
+                    if (OWN) bulk_g2s(st[ks].g, P.gsrc[self] + I.flat_off, ng, full + ks);
+                    if (++ks == SS) { ks = 0; ps ^= 1; }
+                    si += stride;
+                }
+                if (!more) break;
+            }
+        }
+        return;
+    }
+    const float gs = P.clip ? P.clip->gs : P.grad_scale;
+    const int lane = tid & 31, warp = tid >> 5;
+    int kg = 0, ks = 0;
+    uint32_t pg = 0, ps = 0;
+    for (int64_t it = first; it < P.item_end; it += stride) {
+        const Item I = P.items[it];
+        const GroupConst G = P.groups[I.group];
+        mbar_wait(gfull + kg, pg);
+        mbar_wait(full + ks, ps);
+        float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
+        float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
+        float sw = 0.f, su = 0.f;
+        for (int c = tid; c < I.n_chunk; c += kTmaConsumers) {
+            uint2 raw[NS];
+#pragma unroll
+            for (int j = 0, q = 0; j < NS; ++j) {
+                if (OWN && j == self) raw[j] = st[ks].g[c];
+                else raw[j] = gr[kg].g[q++][c];
+            }
+            float4 m = st[ks].m[c], v = st[ks].v[c];
+            const float4 w = st[ks].w[c];
+            chunk_a(sum_raw<NS>(raw), m, v, w, gs, G, sw, su);   // fp32 sum in rank order (Z11)
+            __stcs(mp + c, m);
+            __stcs(vp + c, v);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(gempty + kg);
+            mbar_arrive(empty + ks);
+        }
+        const double dw = warp_sum((double)sw), du = warp_sum((double)su);
+        if (lane == 0) {
+            red_w[warp] = dw;
+            red_u[warp] = du;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
+        if (tid == 0) {
+            double a = 0.0, b = 0.0;
+            for (int q = 0; q < kTmaConsumers / 32; ++q) {
+                a += red_w[q];
+                b += red_u[q];
+            }
+            P.partials[it] = make_double2(a, b);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
+        if (++kg == GS) { kg = 0; pg ^= 1; }
+        if (++ks == SS) { ks = 0; ps ^= 1; }
+    }
+}
+
 // ------------------------------------------------------------ pass B
 __device__ __forceinline__ uint2 chunk_b(const float4 m, const float4 v, float4& w, float scale,
                                          const GroupConst& G) {
@@ -950,7 +1094,10 @@ struct Tune {
     int ring = 0;          // FUSED (NS >= 2): cp.async smem ring of this depth (0 = off)
     int tma = 1;           // D = 1: TMA bulk-copy passes (r01: pass A 98.1 % -> 99.9 % of HBM)
     int tma_multi = 1;     // FUSED D >= 2: TMA passes (peer gradient slices pulled by bulk copies;
-                           // r01: step -4.1 % at D = 2, -3.7 % at D = 4, profiles/r01/sweep_tma.jsonl)
+                           // r01: step -4.1 % at D = 2, -3.7 % at D = 4, profiles/r01/sweep_tma.jsonl);
+                           // at D = 2 pass A uses the decoupled remote-gradient ring (tmam=4:
+                           // pass A -6 %, step -3.5 %; at D = 4 it is 2 % slower than the single
+                           // ring, which stays there; profiles/r01/sweep_tma2_ring.jsonl)
 };
 static Tune g_tune = [] {
     Tune t;
@@ -1007,11 +1154,44 @@ static cudaError_t pass_a_tma(const StepParams& p, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int NS, int SS, bool OWN>
+static cudaError_t pass_a_tma2(const StepParams& p, int grid, cudaStream_t s) {
+    constexpr int NR = OWN ? NS - 1 : NS;
+    constexpr int GS = tma2_grad_stages<NS, SS, OWN>();
+    const size_t smem = sizeof(TmaStateStage<OWN>) * SS + sizeof(TmaGradStage<NR>) * GS + 2 * (SS + GS) * sizeof(uint64_t);
+    static const bool attr = [&] {
+        cudaFuncSetAttribute(pass_a_tma2_kernel<NS, SS, OWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+    }();
+    (void)attr;
+    pass_a_tma2_kernel<NS, SS, OWN><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 template <int NS>
 static cudaError_t pass_a_ns(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
+    if constexpr (NS == 2) {
+        if (t.tma_multi == 1) return pass_a_tma2<NS, 2, true>(p, grid, s);   // the D = 2 default
+        // (tmam=6: the single ring at D = 2, for A/B runs)
+    }
+    if constexpr (NS >= 2 && NS <= 4) {
+        // tmam=2: state ring 3 deep at D = 2 (2 beyond); tmam=3: state ring 2 deep, grads
+        // further ahead (6 items at D = 2); tmam=4/5: own slice in the state ring (2 / 3 deep),
+        // only remote slices in the deep ring
+        if (t.tma_multi == 2) return pass_a_tma2<NS, NS <= 2 ? 3 : 2, false>(p, grid, s);
+        if (t.tma_multi == 3) return pass_a_tma2<NS, 2, false>(p, grid, s);
+        if (t.tma_multi == 4) return pass_a_tma2<NS, 2, true>(p, grid, s);
+        if constexpr (NS == 2) {
+            if (t.tma_multi == 5) return pass_a_tma2<NS, 3, true>(p, grid, s);
+        }
+    }
     if constexpr (NS >= 1) {
         if (NS == 1 ? t.tma : t.tma_multi) return pass_a_tma<NS>(p, grid, s);
+    }
+    if constexpr (NS == 2) {
+        if (t.tma_multi == 1) return pass_a_tma2<NS, 2, true>(p, grid, s);   // the D = 2 default
+        // (tmam=6: the single ring at D = 2, for A/B runs)
     }
     if constexpr (NS >= 2 && NS <= 4) {
         if (t.ring == 3) return pass_a_ring<NS, 4, 3>(p, grid, s);

@@ -82,6 +82,7 @@ struct StepParams {
     float* g32_out;           // grad_stats: materialise the fp32 reduced sums here (FUSED + clip)
     __nv_bfloat16* pdst[LAMB_MAX_RANKS];   // param buffers pass B stores into
     const GroupConst* groups;  // device table [n_groups], refreshed each step by the prologue
+    int32_t self_src;          // index of this rank's own (local) source in gsrc
 };
 
 struct FinalizeParams {
