@@ -683,12 +683,25 @@ struct TmaStageB {
     float4 m[kTmaItem / 4], v[kTmaItem / 4], w[kTmaItem / 4];
 };
 
-template <int ND>
+// BULK: the item's bf16 params are staged in shared memory (one 8 KB buffer per ring stage) and
+// written to every destination param buffer (this rank's and, fused AG, each peer's) with one
+// bulk copy each (cp.async.bulk global<-shared, TMA engine) instead of 8 B STGs per lane.
+struct TmaParamStage {
+    uint2 p[kTmaItem / 4];
+};
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes) : "memory");
+}
+
+template <int ND, bool BULK>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const __grid_constant__ StepParams P) {
     extern __shared__ __align__(128) unsigned char tma_smem_b[];
     TmaStageB* st = reinterpret_cast<TmaStageB*>(tma_smem_b);
     uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem_b + sizeof(TmaStageB) * kTmaStages);
     uint64_t* empty = full + kTmaStages;
+    TmaParamStage* pst = reinterpret_cast<TmaParamStage*>(tma_smem_b + sizeof(TmaStageB) * kTmaStages +
+                                                          2 * kTmaStages * sizeof(uint64_t) + 64);
     const int tid = threadIdx.x;
     if (P.clip && P.clip->skip) return;
     if (tid == 0) {
@@ -730,12 +743,32 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const
             float4 w = st[k].w[c];
             const uint2 pb = chunk_b(st[k].m[c], st[k].v[c], w, scale, G);
             __stcs(wp + c, w);
+            if constexpr (BULK) {
+                pst[k].p[c] = pb;
+            } else {
 #pragma unroll
-            for (int j = 0; j < ND; ++j) __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c, pb);
+                for (int j = 0; j < ND; ++j) __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c, pb);
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + k);
+        if constexpr (BULK) {
+            // the generic-proxy smem writes must be visible to the bulk copy (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
+            if (tid == 0) {
+#pragma unroll
+                for (int j = 0; j < ND; ++j) bulk_s2g(P.pdst[j] + I.flat_off, pst[k].p, (uint32_t)I.n_chunk * 8u);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                // the buffer of the item before this one may be rewritten from the next item's
+                // barrier on (stage k+2 mod 3 is written two items later, after two barriers)
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+        }
         if (++k == kTmaStages) { k = 0; phase ^= 1; }
+    }
+    if constexpr (BULK) {
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // writes performed
     }
     if constexpr (ND > 1) __threadfence_system();   // peer stores visible before the barrier
 }
@@ -1092,6 +1125,7 @@ struct Tune {
     int ua = 4, ma = 2, ub = 4, mb = 2;
     int pf = 1, upf = 4;   // FUSED (NS >= 2): prefetching pass A (U = 4 for NS = 2, else 2; r01 sweep)
     int ring = 0;          // FUSED (NS >= 2): cp.async smem ring of this depth (0 = off)
+    int tmb = 0;           // pass B TMA variant with bulk (TMA-engine) param stores
     int tma = 1;           // D = 1: TMA bulk-copy passes (r01: pass A 98.1 % -> 99.9 % of HBM)
     int tma_multi = 1;     // FUSED D >= 2: TMA passes (peer gradient slices pulled by bulk copies;
                            // r01: step -4.1 % at D = 2, -3.7 % at D = 4, profiles/r01/sweep_tma.jsonl);
@@ -1102,8 +1136,8 @@ struct Tune {
 static Tune g_tune = [] {
     Tune t;
     if (const char* e = getenv("LAMB_TUNE")) {
-        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d,ring=%d,tma=%d,tmam=%d", &t.ua, &t.ma, &t.ub, &t.mb,
-               &t.pf, &t.upf, &t.ring, &t.tma, &t.tma_multi);
+        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d,ring=%d,tma=%d,tmam=%d,tmb=%d", &t.ua, &t.ma, &t.ub,
+               &t.mb, &t.pf, &t.upf, &t.ring, &t.tma, &t.tma_multi, &t.tmb);
     }
     return t;
 }();
@@ -1234,22 +1268,24 @@ static cudaError_t pass_b_v(const StepParams& p, int grid, cudaStream_t s) {
     pass_b_kernel<ND, U, M><<<grid, kThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
-template <int ND>
+template <int ND, bool BULK>
 static cudaError_t pass_b_tma(const StepParams& p, int grid, cudaStream_t s) {
-    const size_t smem = sizeof(TmaStageB) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
+    const size_t smem = sizeof(TmaStageB) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t) + 64 +
+                        (BULK ? sizeof(TmaParamStage) * kTmaStages : 0);
     static const bool attr = [&] {
-        cudaFuncSetAttribute(pass_b_tma_kernel<ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(pass_b_tma_kernel<ND, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return true;
     }();
     (void)attr;
-    pass_b_tma_kernel<ND><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
+    pass_b_tma_kernel<ND, BULK><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 template <int ND>
 static cudaError_t pass_b_nd(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
-    if (ND == 1 ? t.tma : t.tma_multi) return pass_b_tma<ND>(p, grid, s);
+    if (t.tmb) return pass_b_tma<ND, true>(p, grid, s);   // bulk param stores (LAMB_TUNE tmb=1)
+    if (ND == 1 ? t.tma : t.tma_multi) return pass_b_tma<ND, false>(p, grid, s);
     if (t.ub == 2 && t.mb == 4) return pass_b_v<ND, 2, 4>(p, grid, s);
     if (t.ub == 2 && t.mb == 3) return pass_b_v<ND, 2, 3>(p, grid, s);
     if (t.ub == 4 && t.mb == 3) return pass_b_v<ND, 4, 3>(p, grid, s);
