@@ -158,8 +158,12 @@ lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void* stream);
 /* COLLECTIVE.  End-to-end variant with HOST buffers: copies `host_grads` (flat bf16,
  * flat_size elements, pinned for full speed) into the grad buffer, runs the step, and copies
  * the full updated bf16 param buffer back into `host_params` (flat_size elements).
- * Consecutive calls form a pipeline on internal streams: the upload of step t+1 and its pass A
- * run while step t's params are downloaded; only pass B waits for that download.  The first
+ * The copies and the update run as a per-bucket pipeline on internal streams (§3.2
+ * P:318-319, overlap per model chunk): bucket b's upload starts once the previous step's pass A
+ * of b released it, b's update (pass A, norms, ratios, pass B — exact per bucket, every tensor
+ * lives in one bucket) once its grads landed and the previous download of b finished, b's
+ * download once its pass B finished; consecutive calls overlap the same way.  With the pre-step
+ * enabled (lamb_set_grad_clip / lamb_set_loss_scale) the whole table is one unit.  The first
  * call is ordered after the work on `stream`; later calls are ordered among themselves (do not
  * interleave with lamb_step without synchronising).  `host_grads` must hold the gradients when
  * the call is made and stay unchanged until `stream` completes; `stream` completes once
