@@ -12,9 +12,14 @@
 // PAPER.md cites: LAMB §3.1; ZeRO-2 RS/AG §2, §3.2 P:312-328.
 //
 // All three are HBM/NVLink streaming kernels (~1 flop/B): no tensor cores.  Design for B200:
-// 128-bit coalesced streaming loads/stores (ld/st.global.cs, evict-first), several independent
-// chunks per lane in flight, a persistent grid of (148 x resident CTAs) warps walking the item
-// table (profiles/r01_final.md: 97.5 % / 97.4 % of the measured HBM copy bandwidth).
+// the default passes are persistent (one CTA per SM) TMA pipelines — a producer warp streams
+// whole work items into a shared-memory ring with 1-D bulk copies (cp.async.bulk + mbarrier
+// complete_tx; for D > 1 the bulk copies pull the peers' gradient slices over NVLink), eight
+// consumer warps compute and store with 16 B streaming STGs (profiles/r01_tma.md: 99.3 % /
+// 102.5 % of the measured HBM copy bandwidth at D = 1).  At D = 2 pass A keeps the peers'
+// slices in a separate, deeper ring (pass_a_tma2_kernel).  The LDG/STG kernels (128-bit
+// coalesced ld/st.global.cs, several chunks per lane in flight, profiles/r01_final.md) remain
+// as LAMB_TUNE variants and serve the NCCL-mode fp32 input.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -356,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 2) pass_a_ring_kernel(const __grid_c
     }
 }
 
-// ------------------------------------------------------------ pass A, TMA variant (D = 1)
+// ------------------------------------------------------------ pass A, TMA variant (default, any D)
 // One producer warp stages whole items (g 8 B, m/v/w 16 B per 4-element chunk) into a 3-stage
 // shared-memory ring with 1-D bulk copies (cp.async.bulk, TMA engine; mbarrier complete_tx);
 // 8 consumer warps compute from shared memory and store m, v with 16 B STGs.  Tunable
@@ -676,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_b_kernel(const __grid_con
     if constexpr (ND > 1) __threadfence_system();   // peer stores visible before the barrier
 }
 
-// ------------------------------------------------------------ pass B, TMA variant (D = 1)
+// ------------------------------------------------------------ pass B, TMA variant (default, any D)
 // Same ring as pass A's TMA variant: the producer stages m, v, w of an item; consumers recompute
 // u, store w (16 B) and p (8 B) with streaming STGs.
 struct TmaStageB {
