@@ -73,6 +73,9 @@ typedef struct {
 #define LAMB_FLAG_TIMING 1   /* record CUDA events around every phase (lamb_timing_*) */
 #define LAMB_FLAG_GRAPH 2    /* lamb_step replays one captured CUDA graph of the whole step
                                 (D = 1 and FUSED, library grad buffer; no per-phase timing) */
+#define LAMB_FLAG_CE 4       /* FUSED, D > 1: also set up the copy-engine schedule
+                                (lamb_push_grads_bucket / lamb_step_staged /
+                                lamb_wait_params_bucket): a (D-1) x shard bf16 staging buffer */
 
 typedef struct {
     int32_t world_size;        /* D >= 1, <= LAMB_MAX_RANKS; D = 1 needs no unique id */
@@ -200,6 +203,31 @@ lamb_status lamb_sm_partition(int32_t device, int32_t lamb_sms, void** lamb_stre
 /* Deferred all-gather of one bucket's bf16 params (FUSED: NVLink pull of the D-1 peer slices;
  * NCCL: ncclAllGather, COLLECTIVE).  No-op at D = 1. */
 lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream);
+
+/* ---------------- copy-engine schedule (§3.2, on B200) ----------------
+ * The paper overlaps the DP reduce-scatter with the backward and the all-gather with the next
+ * forward.  Here the transfers ride the copy engines (DMA over NVLink, no SMs), so the compute
+ * keeps every SM; the LAMB math then runs after the backward on local HBM only.  Needs
+ * LAMB_FLAG_CE at create (FUSED, D > 1).  Results are bit-identical to lamb_step (same sums in
+ * the same rank order).  EUNSUPPORTED: handle without LAMB_FLAG_CE, or the pre-step enabled.
+ *
+ * lamb_push_grads_bucket — COLLECTIVE per bucket, called as soon as the backward has written
+ *   bucket b's gradients into the library grad buffer (ordered after the work on `stream`):
+ *   copies this rank's gradients of every peer's slice of b into that peer's staging buffer
+ *   (one cudaMemcpyAsync per peer on an internal copy stream) and raises the peer's arrival
+ *   flag (value `step`).  Buckets may be pushed in any order (backward order is the natural).
+ * lamb_step_staged — COLLECTIVE, after every bucket was pushed: `stream` waits (device-side,
+ *   bounded by LAMB_BARRIER_TIMEOUT_MS) until all peers' slices of step `step` landed, then
+ *   pass A (own slice + D-1 staged slices, local HBM), segmented norms with the straddler
+ *   exchange, pass B into this rank's own param slices; then the copy stream pushes the own
+ *   param slices of every bucket (bucket order) into every peer's param buffer — the
+ *   all-gather, deferred into the next forward.
+ * lamb_wait_params_bucket — before bucket b's forward: `stream` waits until every peer's
+ *   param slice of b from lamb_step_staged(step) landed in this rank's param buffer. */
+lamb_status lamb_push_grads_bucket(lamb_t h, int64_t bucket, int64_t step, void* stream);
+lamb_status lamb_step_staged(lamb_t h, int64_t step, void* stream);
+lamb_status lamb_wait_params_bucket(lamb_t h, int64_t bucket, int64_t step, void* stream);
+
 
 /* COLLECTIVE (barrier-free teardown of this rank's peer mappings and communicator). */
 void lamb_destroy(lamb_t h);

@@ -117,6 +117,20 @@ struct lamb_ctx {
     lamb_status ck_status = LAMB_OK;
     std::string ck_error;
 
+    // copy-engine schedule (LAMB_FLAG_CE, FUSED D > 1): shard-ordered staging of the D-1 peers'
+    // gradient slices (peers push into it), per-(bucket, source) arrival flags in the sync buffer
+    __nv_bfloat16* stage = nullptr;                    // [(D-1) x shard_size], IPC-shared
+    __nv_bfloat16* peer_stage[LAMB_MAX_RANKS] = {};
+    size_t ce_off = 0;                                 // byte offset of the CE flags in sync
+    cudaStream_t ce_stream = nullptr;
+    cudaEvent_t ev_ce_in = nullptr, ev_ce_pushed = nullptr, ev_ce_params = nullptr;
+    bool ce() const { return stage != nullptr; }
+    bool staged_now = false;   // inside lamb_step_staged (step_impl: flag wait + staged sources)
+    // gflag[b * D + j]: rank j's gradient slice of bucket b landed in this rank's staging (value
+    // = step); pflag[b * D + j]: rank j's param slice of bucket b landed in this param buffer
+    uint64_t* gflag(int j) const { return reinterpret_cast<uint64_t*>((j < 0 ? sync : peer_sync[j]) + ce_off); }
+    uint64_t* pflag(int j) const { return gflag(j) + (size_t)plan.n_buckets() * cfg.world_size; }
+
     uint64_t* flags(int j) const { return reinterpret_cast<uint64_t*>(peer_sync[j]); }
     uint64_t* epoch() const { return reinterpret_cast<uint64_t*>(sync + 8 * LAMB_MAX_RANKS); }
     // sync buffer layout: [0,64) barrier flags, [64,72) epoch, [128,192) clip rows (double[8]),

@@ -137,8 +137,9 @@ static void free_ctx(lamb_ctx* h) {
         if (h->peer_grad[j] && h->peer_grad[j] != h->grad) cudaIpcCloseMemHandle(h->peer_grad[j]);
         if (h->peer_param[j] && h->peer_param[j] != h->param) cudaIpcCloseMemHandle(h->peer_param[j]);
         if (h->peer_sync[j] && h->peer_sync[j] != h->sync) cudaIpcCloseMemHandle(h->peer_sync[j]);
+        if (h->peer_stage[j]) cudaIpcCloseMemHandle(h->peer_stage[j]);
     }
-    void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->items_b, h->partials, h->segs, h->scale,
+    void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->items_b, h->stage, h->partials, h->segs, h->scale,
                     h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
                     h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_clip_blocks, h->d_groups, h->d_shard_pad, h->d_flat_pad, h->d_check, h->d_tensor_off, h->d_numel,
                     h->d_shard_base, h->d_bucket_base, h->d_bucket_slice};
@@ -149,10 +150,10 @@ static void free_ctx(lamb_ctx* h) {
     for (auto* vec : {&h->ev_rs, &h->ev_b, &h->tev, &h->ev_hb, &h->ev_gf, &h->ev_pb, &h->ev_db})
         for (cudaEvent_t e : *vec) cudaEventDestroy(e);
     for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_grad_free, h->ev_h2d, h->ev_params, h->ev_d2h,
-                          h->ev_call, h->ev_fork, h->ev_join})
+                          h->ev_call, h->ev_fork, h->ev_join, h->ev_ce_in, h->ev_ce_pushed, h->ev_ce_params})
         if (e) cudaEventDestroy(e);
     for (cudaStream_t st : {h->comm_stream, h->h2d_stream, h->d2h_stream, h->work_stream, h->cap_stream,
-                            h->x_stream})
+                            h->x_stream, h->ce_stream})
         if (st) cudaStreamDestroy(st);
     if (h->comm) ncclCommDestroy(h->comm);
     delete h;
@@ -315,25 +316,31 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
         h->peer_sync[j] = h->sync;
     }
     if (h->cfg.comm_mode != LAMB_COMM_FUSED) return LAMB_OK;
-    // exchange IPC handles of grad / param / sync through NCCL (one all-gather)
-    cudaIpcMemHandle_t mine[3];
+    // exchange IPC handles of grad / param / sync (+ the CE staging) in one all-gather
+    cudaIpcMemHandle_t mine[4];
+    const int nh = h->ce() ? 4 : 3;
     CUDA_TRY(h, cudaIpcGetMemHandle(&mine[0], h->grad));
     CUDA_TRY(h, cudaIpcGetMemHandle(&mine[1], h->param));
     CUDA_TRY(h, cudaIpcGetMemHandle(&mine[2], h->sync));
-    std::vector<cudaIpcMemHandle_t> all(3 * D);
+    if (h->ce()) CUDA_TRY(h, cudaIpcGetMemHandle(&mine[3], h->stage));
+    std::vector<cudaIpcMemHandle_t> all((size_t)nh * D);
     {
-        lamb_status st = bootstrap_allgather(h, mine, all.data(), sizeof(mine));
+        lamb_status st = bootstrap_allgather(h, mine, all.data(), sizeof(cudaIpcMemHandle_t) * nh);
         if (st != LAMB_OK) return st;
     }
     for (int j = 0; j < D; ++j) {
         if (j == r) continue;
         void* p = nullptr;
-        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[3 * j + 0], cudaIpcMemLazyEnablePeerAccess));
+        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 0], cudaIpcMemLazyEnablePeerAccess));
         h->peer_grad[j] = static_cast<__nv_bfloat16*>(p);
-        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[3 * j + 1], cudaIpcMemLazyEnablePeerAccess));
+        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 1], cudaIpcMemLazyEnablePeerAccess));
         h->peer_param[j] = static_cast<__nv_bfloat16*>(p);
-        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[3 * j + 2], cudaIpcMemLazyEnablePeerAccess));
+        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 2], cudaIpcMemLazyEnablePeerAccess));
         h->peer_sync[j] = static_cast<char*>(p);
+        if (h->ce()) {
+            CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 3], cudaIpcMemLazyEnablePeerAccess));
+            h->peer_stage[j] = static_cast<__nv_bfloat16*>(p);
+        }
     }
     // make sure every rank has mapped everything before the first step
     CUDA_TRY(h, cudaDeviceSynchronize());
@@ -441,6 +448,14 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
     CUDA_STEP(cudaMemset(h->v, 0, (size_t)p.shard_size * 4));
     STEP(build_tables(h));
     h->sync_bytes = 256 + sizeof(double2) * (size_t)D * std::max<size_t>(1, p.straddlers.size());
+    const bool want_ce = D > 1 && cfg->comm_mode == LAMB_COMM_FUSED && (cfg->flags & LAMB_FLAG_CE);
+    if (want_ce) {
+        // copy-engine schedule: arrival flags after the straddler rows; the staging buffer
+        h->ce_off = (h->sync_bytes + 63) & ~(size_t)63;
+        h->sync_bytes = h->ce_off + 2 * sizeof(uint64_t) * (size_t)p.n_buckets() * D;
+        CUDA_STEP(dalloc(&h->stage, (size_t)(D - 1) * (size_t)p.shard_size));
+        CUDA_STEP(cudaMemset(h->stage, 0, (size_t)(D - 1) * (size_t)p.shard_size * 2));
+    }
     CUDA_STEP(dalloc(&h->sync, h->sync_bytes));
     CUDA_STEP(cudaMemset(h->sync, 0, h->sync_bytes));
     CUDA_STEP(dalloc(&h->d_clip, 1));
@@ -468,6 +483,11 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
             CUDA_STEP(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
             const char* e = getenv("LAMB_NO_STRAD_HIDE");
             h->no_strad_hide = e && *e && *e != '0';
+            if (h->ce()) {
+                CUDA_STEP(cudaStreamCreateWithFlags(&h->ce_stream, cudaStreamNonBlocking));
+                for (cudaEvent_t* e2 : {&h->ev_ce_in, &h->ev_ce_pushed, &h->ev_ce_params})
+                    CUDA_STEP(cudaEventCreateWithFlags(e2, cudaEventDisableTiming));
+            }
         }
         if (cfg->comm_mode == LAMB_COMM_NCCL) {
             CUDA_STEP(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
@@ -615,10 +635,21 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         // ---------------- D = 1 or FUSED
         uint64_t* flags[LAMB_MAX_RANKS];
         for (int j = 0; j < D; ++j) flags[j] = h->flags(j);
-        if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
+        if (h->staged_now) {
+            // copy-engine schedule: every peer's slices of this step landed in the staging
+            LAUNCH(h, lamb::launch_flag_wait(h->gflag(-1), b0, b1, D, r, (uint64_t)t, h->err_flag_dev,
+                                             h->barrier_timeout_ns, s));
+        } else if (fused) {
+            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
+        }
         mark(h, 1, s);
         for (int j = 0; j < D; ++j)
             sp.gsrc[j] = fused ? h->peer_grad[j] : (grads ? (const __nv_bfloat16*)grads : h->grad);
+        if (h->staged_now) {
+            for (int j = 0; j < D; ++j)
+                sp.gsrc[j] = j == r ? h->grad : h->stage + (size_t)(j - (j > r)) * (size_t)p.shard_size;
+            sp.staged = 1;
+        }
         if (fused && h->diag_local_grads)   // timing diagnostic only (wrong sums): no NVLink loads
             for (int j = 0; j < D; ++j) sp.gsrc[j] = h->grad;
         if (pre) {
@@ -871,6 +902,87 @@ extern "C" lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream
     }
     NCCL_TRY(h, ncclAllGather(h->param + base + (int64_t)r * sl, h->param + base, (size_t)sl,
                               ncclBfloat16, h->comm, s));
+    return LAMB_OK;
+}
+
+// ------------------------------------------------------------------ copy-engine schedule
+static lamb_status ce_check(lamb_ctx* h, int64_t bucket, int64_t step) {
+    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
+    if (!h->ce()) return fail(h, LAMB_EUNSUPPORTED, "handle created without LAMB_FLAG_CE (FUSED, D > 1)");
+    if (bucket < -1 || bucket >= h->plan.n_buckets()) return fail(h, LAMB_EINVAL, "bucket out of range");
+    if (step < 1) return fail(h, LAMB_EINVAL, "step must be >= 1");
+    if (h->prestep()) return fail(h, LAMB_EUNSUPPORTED, "the pre-step needs lamb_step (global norm before pass A)");
+    return check_async(h);
+}
+
+extern "C" lamb_status lamb_push_grads_bucket(lamb_t h, int64_t bucket, int64_t step, void* stream) {
+    lamb_status st = ce_check(h, bucket, step);
+    if (st != LAMB_OK) return st;
+    if (bucket < 0) return fail(h, LAMB_EINVAL, "bucket out of range");
+    cudaSetDevice(h->device);
+    const Plan& p = h->plan;
+    const int D = p.world, r = p.rank;
+    const int64_t base = p.buckets[4 * bucket], sl = p.buckets[4 * bucket + 1] / D, sb = p.shard_base[bucket];
+    CUDA_TRY(h, cudaEventRecord(h->ev_ce_in, static_cast<cudaStream_t>(stream)));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->ce_stream, h->ev_ce_in, 0));
+    uint64_t* fl[LAMB_MAX_RANKS];
+    int nf = 0;
+    for (int j = 0; j < D; ++j) {
+        if (j == r) continue;
+        // peer j's staging slot for source r, at j's (= every rank's) shard offset of bucket b
+        __nv_bfloat16* dst = h->peer_stage[j] + (size_t)(r - (r > j)) * (size_t)p.shard_size + sb;
+        CUDA_TRY(h, cudaMemcpyAsync(dst, h->grad + base + (int64_t)j * sl, (size_t)sl * 2, cudaMemcpyDefault,
+                                    h->ce_stream));
+        fl[nf++] = h->gflag(j) + bucket * D + r;
+    }
+    LAUNCH(h, lamb::launch_flag_store(fl, nf, (uint64_t)step, h->ce_stream));
+    CUDA_TRY(h, cudaEventRecord(h->ev_ce_pushed, h->ce_stream));
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_step_staged(lamb_t h, int64_t step, void* stream) {
+    lamb_status st = ce_check(h, -1, step);
+    if (st != LAMB_OK) return st;
+    if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step_staged before lamb_set_master / lamb_synth_init");
+    cudaSetDevice(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Plan& p = h->plan;
+    const int D = p.world, r = p.rank;
+    // the grad buffer is rewritten by the next backward: this rank's pushes must have read it
+    CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_ce_pushed, 0));
+    st = prologue(h, step, s);
+    if (st != LAMB_OK) return st;
+    h->staged_now = true;
+    st = step_impl(h, nullptr, step, s, 0, p.n_buckets(), /*defer_ag=*/true);
+    h->staged_now = false;
+    if (h->t_n < h->t_max) ++h->t_n;
+    if (st != LAMB_OK) return st;
+    // the all-gather on the copy engines, bucket order (the next forward's order)
+    CUDA_TRY(h, cudaEventRecord(h->ev_ce_params, s));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->ce_stream, h->ev_ce_params, 0));
+    for (int64_t b = 0; b < p.n_buckets(); ++b) {
+        const int64_t base = p.buckets[4 * b], sl = p.buckets[4 * b + 1] / D;
+        const int64_t off = base + (int64_t)r * sl;
+        uint64_t* fl[LAMB_MAX_RANKS];
+        int nf = 0;
+        for (int j = 0; j < D; ++j) {
+            if (j == r) continue;
+            CUDA_TRY(h, cudaMemcpyAsync(h->peer_param[j] + off, h->param + off, (size_t)sl * 2, cudaMemcpyDefault,
+                                        h->ce_stream));
+            fl[nf++] = h->pflag(j) + b * D + r;
+        }
+        LAUNCH(h, lamb::launch_flag_store(fl, nf, (uint64_t)step, h->ce_stream));
+    }
+    return LAMB_OK;
+}
+
+extern "C" lamb_status lamb_wait_params_bucket(lamb_t h, int64_t bucket, int64_t step, void* stream) {
+    lamb_status st = ce_check(h, bucket, step);
+    if (st != LAMB_OK) return st;
+    if (bucket < 0) return fail(h, LAMB_EINVAL, "bucket out of range");
+    cudaSetDevice(h->device);
+    LAUNCH(h, lamb::launch_flag_wait(h->pflag(-1), bucket, bucket + 1, h->plan.world, h->plan.rank, (uint64_t)step,
+                                     h->err_flag_dev, h->barrier_timeout_ns, static_cast<cudaStream_t>(stream)));
     return LAMB_OK;
 }
 

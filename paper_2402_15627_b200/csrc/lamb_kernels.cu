@@ -430,7 +430,9 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
                 const uint32_t nf = (uint32_t)I.n_chunk * 16u, ng = (uint32_t)I.n_chunk * 8u;
                 mbar_expect_tx(full + k, 3 * nf + NS * ng);
 #pragma unroll
-                for (int j = 0; j < NS; ++j) bulk_g2s(st[k].g[j], P.gsrc[j] + I.flat_off, ng, full + k);
+                for (int j = 0; j < NS; ++j)
+                    bulk_g2s(st[k].g[j], P.gsrc[j] + ((P.staged && j != P.self_src) ? I.shard_off : I.flat_off), ng,
+                             full + k);
                 bulk_g2s(st[k].m, P.m + I.shard_off, nf, full + k);
                 bulk_g2s(st[k].v, P.v + I.shard_off, nf, full + k);
                 bulk_g2s(st[k].w, P.w + I.shard_off, nf, full + k);
@@ -555,7 +557,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
 #pragma unroll
                     for (int j = 0, q = 0; j < NS; ++j) {
                         if (OWN && j == self) continue;
-                        bulk_g2s(gr[kg].g[q++], P.gsrc[j] + I.flat_off, ng, gfull + kg);
+                        bulk_g2s(gr[kg].g[q++], P.gsrc[j] + ((P.staged && j != self) ? I.shard_off : I.flat_off), ng,
+                                 gfull + kg);
                     }
                     if (++kg == GS) { kg = 0; pg ^= 1; }
                 }
@@ -1030,6 +1033,34 @@ __global__ void gather_kernel(const __grid_constant__ GatherArgs A, __nv_bfloat1
     }
 }
 
+// ------------------------------------------------------------ copy-engine schedule flags
+struct FlagArgs {
+    uint64_t* p[LAMB_MAX_RANKS];
+};
+__global__ void flag_store_kernel(const __grid_constant__ FlagArgs A, int n, uint64_t v) {
+    const int i = threadIdx.x;
+    if (i < n) {
+        __threadfence_system();
+        st_release_sys(A.p[i], v);
+    }
+}
+__global__ void flag_wait_kernel(const uint64_t* flags, int64_t b0, int64_t b1, int world, int rank, uint64_t v,
+                                 int* err, uint64_t timeout_ns) {
+    const int64_t n = (b1 - b0) * world;
+    const uint64_t t0 = globaltimer();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        if ((int)(i % world) == rank) continue;
+        const uint64_t* f = flags + b0 * world + i;
+        while (ld_acquire_sys(f) < v) {
+            if (globaltimer() - t0 > timeout_ns) {
+                atomicExch(err, 1);
+                return;
+            }
+            __nanosleep(128);
+        }
+    }
+}
+
 // ------------------------------------------------------------ casts
 __global__ void upcast_bf16_kernel(const __nv_bfloat16* __restrict__ src, float* __restrict__ dst,
                                    int64_t n) {
@@ -1210,6 +1241,12 @@ static cudaError_t pass_a_tma2(const StepParams& p, int grid, cudaStream_t s) {
 template <int NS>
 static cudaError_t pass_a_ns(const StepParams& p, int grid, cudaStream_t s) {
     const Tune& t = g_tune;
+    if constexpr (NS >= 2) {
+        if (p.staged) {   // copy-engine schedule: only the TMA kernels address staging by shard offset
+            if constexpr (NS == 2) return pass_a_tma2<NS, 2, true>(p, grid, s);
+            else return pass_a_tma<NS>(p, grid, s);
+        }
+    }
     if constexpr (NS == 2) {
         if (t.tma_multi == 1) return pass_a_tma2<NS, 2, true>(p, grid, s);   // the D = 2 default
         // (tmam=6: the single ring at D = 2, for A/B runs)
@@ -1403,6 +1440,20 @@ cudaError_t launch_barrier(uint64_t* const* flags, uint64_t* epoch, int rank, in
     BarrierArgs a;
     for (int j = 0; j < LAMB_MAX_RANKS; ++j) a.flags[j] = j < world ? flags[j] : nullptr;
     barrier_kernel_v<<<1, 32, 0, s>>>(a, epoch, rank, world, err_flag, timeout_ns);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flag_store(uint64_t* const* ptrs, int n, uint64_t v, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    FlagArgs a;
+    for (int j = 0; j < LAMB_MAX_RANKS; ++j) a.p[j] = j < n ? ptrs[j] : nullptr;
+    flag_store_kernel<<<1, 32, 0, s>>>(a, n, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flag_wait(const uint64_t* flags, int64_t b0, int64_t b1, int world, int rank, uint64_t v,
+                             int* err_flag, uint64_t timeout_ns, cudaStream_t s) {
+    flag_wait_kernel<<<1, 256, 0, s>>>(flags, b0, b1, world, rank, v, err_flag, timeout_ns);
     return cudaGetLastError();
 }
 

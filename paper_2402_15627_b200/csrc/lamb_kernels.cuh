@@ -83,6 +83,8 @@ struct StepParams {
     __nv_bfloat16* pdst[LAMB_MAX_RANKS];   // param buffers pass B stores into
     const GroupConst* groups;  // device table [n_groups], refreshed each step by the prologue
     int32_t self_src;          // index of this rank's own (local) source in gsrc
+    int32_t staged;            // 1: sources j != self_src are shard-ordered staging buffers
+                               // (copy-engine schedule): addressed by shard_off, not flat_off
 };
 
 struct FinalizeParams {
@@ -132,6 +134,11 @@ cudaError_t launch_barrier(uint64_t* const* flags, uint64_t* epoch, int rank, in
                            int* err_flag, cudaStream_t s, uint64_t timeout_ns);
 cudaError_t launch_gather(const __nv_bfloat16* const* peers, __nv_bfloat16* dst, int64_t base, int64_t slice,
                           int world, int rank, cudaStream_t s);
+// copy-engine schedule: raise flags (system-scope release stores, e.g. in peers' sync buffers)
+// and wait for flags[(b * world + j)] >= v for b in [b0, b1), j != rank (bounded; err on timeout)
+cudaError_t launch_flag_store(uint64_t* const* ptrs, int n, uint64_t v, cudaStream_t s);
+cudaError_t launch_flag_wait(const uint64_t* flags, int64_t b0, int64_t b1, int world, int rank, uint64_t v,
+                             int* err_flag, uint64_t timeout_ns, cudaStream_t s);
 cudaError_t launch_upcast_bf16(const __nv_bfloat16* src, float* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_cast_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t s);
 int pass_grid(int device, int nsrc, bool g32, bool pass_b, int ndst);

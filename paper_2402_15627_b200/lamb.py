@@ -30,6 +30,7 @@ LAMB_UNIQUE_ID_BYTES = 128
 LAMB_COMM_NCCL, LAMB_COMM_FUSED = 0, 1
 LAMB_FLAG_TIMING = 1
 LAMB_FLAG_GRAPH = 2
+LAMB_FLAG_CE = 4
 LAMB_BUCKET_DEFER_AG = 1
 LAMB_BUF_GRAD, LAMB_BUF_PARAM, LAMB_BUF_W, LAMB_BUF_M, LAMB_BUF_V, LAMB_BUF_GSUM = range(6)
 PHASES = ["barrier_in", "pass_a", "finalize", "exchange", "pass_b", "barrier_out"]
@@ -91,6 +92,9 @@ _SIGS = {
     "lamb_step_host": (_st, [_vp, _vp, _vp, ctypes.c_int64, _vp]),
     "lamb_step_bucket": (_st, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _vp]),
     "lamb_gather_bucket": (_st, [_vp, ctypes.c_int64, _vp]),
+    "lamb_push_grads_bucket": (_st, [_vp, ctypes.c_int64, ctypes.c_int64, _vp]),
+    "lamb_step_staged": (_st, [_vp, ctypes.c_int64, _vp]),
+    "lamb_wait_params_bucket": (_st, [_vp, ctypes.c_int64, ctypes.c_int64, _vp]),
     "lamb_set_max_ctas": (_st, [_vp, ctypes.c_int32]),
     "lamb_self_check": (_st, [_vp, _vp, _vp]),
     "lamb_sm_partition": (_st, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
@@ -213,7 +217,7 @@ class Lamb:
     def __init__(self, tensors: Sequence[tuple], groups: Sequence, world_size: int = 1, rank: int = 0,
                  device: int = 0, comm_mode: int = LAMB_COMM_FUSED, bucket_cap: int = 0,
                  grad_scale: float = 0.0, timing: bool = False, unique_id: Optional[bytes] = None,
-                 pg=None, graph: bool = False, bootstrap: str = "nccl"):
+                 pg=None, graph: bool = False, bootstrap: str = "nccl", ce: bool = False):
         import torch
         self.torch = torch
         self.device = device
@@ -229,7 +233,8 @@ class Lamb:
             garr[k].eps, garr[k].weight_decay = get("eps"), get("weight_decay")
             garr[k].adapt, garr[k].bias_correction = int(get("adapt")), int(get("bias_correction"))
         cfg = lamb_config(world_size, rank, device, comm_mode, bucket_cap, grad_scale,
-                          (LAMB_FLAG_TIMING if timing else 0) | (LAMB_FLAG_GRAPH if graph else 0))
+                          (LAMB_FLAG_TIMING if timing else 0) | (LAMB_FLAG_GRAPH if graph else 0) |
+                          (LAMB_FLAG_CE if ce else 0))
         self.h = _vp()
         if world_size > 1 and bootstrap == "host":
             # FUSED without an NCCL communicator: IPC handles exchanged over the caller's group
@@ -302,6 +307,17 @@ class Lamb:
 
     def gather_bucket(self, bucket: int, stream=None) -> None:
         check(lamb_gather_bucket(self.h, int(bucket), self._stream(stream)), self.h)
+
+    # copy-engine schedule (ce=True at construction): RS pushes during the backward, the update
+    # after it, the AG pushes into the next forward
+    def push_grads_bucket(self, bucket: int, t: int, stream=None) -> None:
+        check(lamb_push_grads_bucket(self.h, int(bucket), int(t), self._stream(stream)), self.h)
+
+    def step_staged(self, t: int, stream=None) -> None:
+        check(lamb_step_staged(self.h, int(t), self._stream(stream)), self.h)
+
+    def wait_params_bucket(self, bucket: int, t: int, stream=None) -> None:
+        check(lamb_wait_params_bucket(self.h, int(bucket), int(t), self._stream(stream)), self.h)
 
     def step_host(self, host_grads, host_params, t: int, stream=None) -> None:
         check(lamb_step_host(self.h, ctypes.c_void_p(host_grads.data_ptr()),

@@ -271,6 +271,49 @@ def graph_case(world, rank, local, mode):
         print(f"[ok] CUDA-graph step D={world} == eager (bitwise)", flush=True)
 
 
+def ce_case(world, rank, local, mode):
+    """Copy-engine schedule (LAMB_FLAG_CE): gradient pushes per bucket in backward order, the
+    staged update, the param pushes awaited per bucket — bitwise equal to lamb_step (FUSED) over
+    several steps: w, m, v and every rank's full param buffer."""
+    from paper_2402_15627_b200 import lamb
+    if mode != lamb.LAMB_COMM_FUSED:
+        return
+    rng = np.random.default_rng(505)
+    tensors = W.random_table(rng, 50, max_numel=7000, p_big=0.2, big=50_000) + W.stress_tensors(0, 300)
+    wl = W.Workload("ce", 79, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    mk = lambda ce: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
+                              device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD,
+                              bootstrap=BOOT, ce=ce)
+    A, B = mk(True), mk(False)
+    A.synth_init(spec, wl.seed)
+    B.synth_init(spec, wl.seed)
+    nb = A.plan.buckets.shape[0]
+    assert nb > 4 and len(A.plan.straddlers) > 0
+    for t in (1, 2, 3, 4):
+        if t > 1:
+            for b in range(nb):            # the next forward: params of step t-1, bucket order
+                A.wait_params_bucket(b, t - 1)
+        A.synth_grads(spec, wl.seed, rank + 1, t)
+        for b in reversed(range(nb)):      # backward order
+            A.push_grads_bucket(b, t)
+        A.step_staged(t)
+        B.synth_grads(spec, wl.seed, rank + 1, t)
+        B.step(t)
+    for b in range(nb):
+        A.wait_params_bucket(b, 4)
+    torch.cuda.synchronize()
+    for k in (2, 3, 4):
+        assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32)), k
+    assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
+    assert all(v == 0 for v in A.self_check().values()), A.self_check()
+    A.close()
+    B.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] copy-engine schedule D={world} ({nb} buckets, 4 steps) == lamb_step (bitwise)", flush=True)
+
+
 def replicated_case(world, rank, local, mode):
     """H8 on the GPU: every rank feeds the SAME gradients (REPLICATED generator stream), so the
     DP mean is that gradient and the D-rank sharded step must match the UNSHARDED oracle run
@@ -481,6 +524,7 @@ def main():
         ckpt_case(world, rank, local, mode)
         hide_case(world, rank, local, mode)
         replicated_case(world, rank, local, mode)
+        ce_case(world, rank, local, mode)
         dist.barrier()
         dist.destroy_process_group()
         return
@@ -525,6 +569,7 @@ def main():
     h10_case(world, rank, local, mode)
     hide_case(world, rank, local, mode)
     replicated_case(world, rank, local, mode)
+    ce_case(world, rank, local, mode)
     torch_case(world, rank, local, mode)
     os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"
     failure_case(world, rank, local, mode)

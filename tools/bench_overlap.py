@@ -11,6 +11,10 @@ ranks:
   overlap  - per bucket: lamb_step_bucket(b, defer AG) on a second stream as soon as b's
              backward is done; lamb_gather_bucket(b) before b's next forward (prefetched in
              bucket order at the start of the iteration).
+  ce       - the copy-engine schedule (D > 1): lamb_push_grads_bucket(b) right after b's
+             backward (the reduce-scatter traffic on the DMA engines, no SMs), lamb_step_staged
+             after the backward (local-HBM update, then the all-gather pushes on the DMA
+             engines), lamb_wait_params_bucket(b) before b's next forward.
     python tools/bench_overlap.py --config gpt1.3b --tokens 4096
     python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/bench_overlap.py
 """
@@ -53,7 +57,7 @@ if world > 1:
 wl = W.get(a.config)
 spec = [(t.init, t.gexp) for t in wl.tensors]
 L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
-              device=local, bucket_cap=a.cap or wl.cap, pg=pg)
+              device=local, bucket_cap=a.cap or wl.cap, pg=pg, ce=world > 1)
 L.synth_init(spec, wl.seed)
 L.synth_grads(spec, wl.seed, rank + 1, 1)
 B = len(L.plan.buckets)
@@ -79,6 +83,7 @@ ev_grad = [torch.cuda.Event() for _ in range(B)]
 ev_gath = [torch.cuda.Event() for _ in range(B)]
 ev_ls_done = torch.cuda.Event()
 step = [0]
+last_ce = [0]   # last step done by lamb_step_staged (its params are pushed into the next forward)
 
 
 def iteration(mode, comp=comp, ls=ls):
@@ -101,6 +106,16 @@ def iteration(mode, comp=comp, ls=ls):
             L.step_bucket(b, t, defer_ag=True, stream=ls)
         ev_ls_done.record(ls)
         comp.wait_event(ev_ls_done)
+    elif mode == "ce":
+        for b in range(B):
+            if last_ce[0]:
+                L.wait_params_bucket(b, last_ce[0], stream=comp)
+            gemms(reps_f[b])
+        for b in reversed(range(B)):
+            gemms(2 * reps_f[b])
+            L.push_grads_bucket(b, t, stream=comp)
+        L.step_staged(t, stream=comp)
+        last_ce[0] = t
     else:
         for b in range(B):
             gemms(reps_f[b])
@@ -134,8 +149,12 @@ def timed(mode, comp=comp, ls=ls):
 
 
 res = {}
-for m in ("compute", "serial", "serial_buckets"):
+for m in ("compute", "serial", "serial_buckets") + (("ce",) if world > 1 else ()):
     res[m] = timed(m)
+if world > 1:
+    # the first timed "ce" iteration waited on the params of a staged step; re-time after the
+    # other modes ran, then the next "ce" run waits on last_ce again (it is still current)
+    res["ce"] = min(res["ce"], timed("ce"))
 over = {}
 for c in [int(x) for x in a.ctas.split(",")]:
     L.set_max_ctas(c)
@@ -170,7 +189,9 @@ if rank == 0:
                       "ms_compute_on_partition": {k: v for k, v in res.items() if k.startswith("compute_green")},
                       "ms_overlap_by_max_ctas": over, "best_max_ctas": best, "ms_overlap": over[best],
                       "exposed_ms_serial": exposed_serial, "exposed_ms_overlap": exposed_overlap,
-                      "hidden_frac": 1.0 - exposed_overlap / exposed_serial if exposed_serial > 0 else None}))
+                      "hidden_frac": 1.0 - exposed_overlap / exposed_serial if exposed_serial > 0 else None,
+                      "ms_ce": res.get("ce"),
+                      "exposed_ms_ce": (res["ce"] - res["compute"]) if "ce" in res else None}))
 L.close()
 if world > 1:
     dist.barrier()
