@@ -216,10 +216,12 @@ lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream);
  *   copies this rank's gradients of every peer's slice of b into that peer's staging buffer
  *   (one cudaMemcpyAsync per peer on an internal copy stream) and raises the peer's arrival
  *   flag (value `step`).  Buckets may be pushed in any order (backward order is the natural).
- * lamb_step_staged — COLLECTIVE, after every bucket was pushed: `stream` waits (device-side,
- *   bounded by LAMB_BARRIER_TIMEOUT_MS) until all peers' slices of step `step` landed, then
- *   pass A (own slice + D-1 staged slices, local HBM), segmented norms with the straddler
- *   exchange, pass B into this rank's own param slices; then the copy stream pushes the own
+ * lamb_step_staged — COLLECTIVE, after every bucket was pushed: pass A (own slice + D-1 staged
+ *   slices, local HBM) walks the buckets in reverse (the order the backward pushed them) and
+ *   waits in-kernel, per bucket and bounded by LAMB_BARRIER_TIMEOUT_MS, until all peers' slices
+ *   of step `step` landed — so the last bucket's transfer overlaps pass A of the others; then
+ *   segmented norms with the straddler exchange, pass B into this rank's own param slices;
+ *   then the copy stream pushes the own
  *   param slices of every bucket (bucket order) into every peer's param buffer — the
  *   all-gather, deferred into the next forward.
  * lamb_wait_params_bucket — before bucket b's forward: `stream` waits until every peer's

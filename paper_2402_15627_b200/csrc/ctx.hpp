@@ -125,6 +125,7 @@ struct lamb_ctx {
     cudaStream_t ce_stream = nullptr;
     cudaEvent_t ev_ce_in = nullptr, ev_ce_pushed = nullptr, ev_ce_params = nullptr;
     bool ce() const { return stage != nullptr; }
+    int32_t* d_item_bucket = nullptr;   // [n_items] bucket of each item (staged pass A waits)
     bool staged_now = false;   // inside lamb_step_staged (step_impl: flag wait + staged sources)
     // gflag[b * D + j]: rank j's gradient slice of bucket b landed in this rank's staging (value
     // = step); pflag[b * D + j]: rank j's param slice of bucket b landed in this param buffer

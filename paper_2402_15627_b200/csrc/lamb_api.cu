@@ -139,7 +139,7 @@ static void free_ctx(lamb_ctx* h) {
         if (h->peer_sync[j] && h->peer_sync[j] != h->sync) cudaIpcCloseMemHandle(h->peer_sync[j]);
         if (h->peer_stage[j]) cudaIpcCloseMemHandle(h->peer_stage[j]);
     }
-    void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->items_b, h->stage, h->partials, h->segs, h->scale,
+    void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->items_b, h->stage, h->d_item_bucket, h->partials, h->segs, h->scale,
                     h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
                     h->sync, h->g32, h->up32[0], h->up32[1], h->d_clip, h->d_clip_blocks, h->d_groups, h->d_shard_pad, h->d_flat_pad, h->d_check, h->d_tensor_off, h->d_numel,
                     h->d_shard_base, h->d_bucket_base, h->d_bucket_slice};
@@ -221,6 +221,12 @@ static lamb_status build_tables(lamb_ctx* h) {
     h->n_items = (int64_t)items.size();
     h->n_local_strad = (int32_t)ls_slot.size();
     CUDA_TRY(h, upload(&h->items, items));
+    {
+        std::vector<int32_t> ib(items.size());
+        for (int64_t k = 0; k < B; ++k)
+            for (int64_t i = h->bucket_item_begin[k]; i < h->bucket_item_begin[k + 1]; ++i) ib[i] = (int32_t)k;
+        CUDA_TRY(h, upload(&h->d_item_bucket, ib));
+    }
     if (p.world > 1 && h->n_local_strad > 0) {
         // pass B order for the whole-table FUSED step: items of non-straddler tensors first (their
         // trust ratios are final after the local finalize), straddler items last (they wait for the
@@ -636,9 +642,8 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         uint64_t* flags[LAMB_MAX_RANKS];
         for (int j = 0; j < D; ++j) flags[j] = h->flags(j);
         if (h->staged_now) {
-            // copy-engine schedule: every peer's slices of this step landed in the staging
-            LAUNCH(h, lamb::launch_flag_wait(h->gflag(-1), b0, b1, D, r, (uint64_t)t, h->err_flag_dev,
-                                             h->barrier_timeout_ns, s));
+            // copy-engine schedule: pass A waits per bucket for the peers' slices (in-kernel,
+            // walking the buckets in the order the backward pushed them)
         } else if (fused) {
             LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
         }
@@ -649,6 +654,13 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
             for (int j = 0; j < D; ++j)
                 sp.gsrc[j] = j == r ? h->grad : h->stage + (size_t)(j - (j > r)) * (size_t)p.shard_size;
             sp.staged = 1;
+            sp.reverse = 1;
+            sp.world = D;
+            sp.item_bucket = h->d_item_bucket;
+            sp.gflags = h->gflag(-1);
+            sp.gflag_target = (uint64_t)t;
+            sp.err = h->err_flag_dev;
+            sp.timeout_ns = h->barrier_timeout_ns;
         }
         if (fused && h->diag_local_grads)   // timing diagnostic only (wrong sums): no NVLink loads
             for (int j = 0; j < D; ++j) sp.gsrc[j] = h->grad;

@@ -398,6 +398,39 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// Copy-engine schedule: logical position -> item (reverse walk), and the per-bucket arrival wait
+// of the producer thread (system-scope acquire of the peers' flags, bounded).
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ int64_t item_at(const StepParams& P, int64_t k) {
+    return P.reverse ? P.item_end - 1 - (k - P.item_begin) : k;
+}
+__device__ __forceinline__ void wait_bucket_arrivals(const StepParams& P, int64_t ix, int32_t& last_b) {
+    if (!P.gflags) return;
+    const int32_t b = P.item_bucket[ix];
+    if (b == last_b) return;
+    last_b = b;
+    const uint64_t t0 = globaltimer_ns();
+    for (int j = 0; j < P.world; ++j) {
+        if (j == P.self_src) continue;
+        const uint64_t* f = P.gflags + (int64_t)b * P.world + j;
+        uint64_t v;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+            if (v >= P.gflag_target) break;
+            if (globaltimer_ns() - t0 > P.timeout_ns) {
+                atomicExch(P.err, 1);
+                break;
+            }
+            __nanosleep(256);
+        } while (true);
+    }
+    asm volatile("fence.proxy.async;" ::: "memory");   // the bulk copies (async proxy) come next
+}
+
 // NS = 1: D = 1 (local gradients); NS = D >= 2: the fused reduce-scatter — the bulk copies pull
 // each rank's gradient slice of the item (over NVLink for peers) into shared memory.
 template <int NS>
@@ -424,9 +457,12 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
         if (tid == kTmaConsumers) {
             int k = 0;
             uint32_t phase = 0;
+            int32_t last_b = -1;
             for (int64_t it = first; it < P.item_end; it += stride) {
                 mbar_wait(empty + k, phase ^ 1);
-                const Item I = P.items[it];
+                const int64_t ix = item_at(P, it);
+                wait_bucket_arrivals(P, ix, last_b);
+                const Item I = P.items[ix];
                 const uint32_t nf = (uint32_t)I.n_chunk * 16u, ng = (uint32_t)I.n_chunk * 8u;
                 mbar_expect_tx(full + k, 3 * nf + NS * ng);
 #pragma unroll
@@ -447,7 +483,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
     int k = 0;
     uint32_t phase = 0;
     for (int64_t it = first; it < P.item_end; it += stride) {
-        const Item I = P.items[it];
+        const int64_t ix = item_at(P, it);
+        const Item I = P.items[ix];
         const GroupConst G = P.groups[I.group];
         mbar_wait(full + k, phase);
         float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
@@ -477,7 +514,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
                 a += red_w[q];
                 b += red_u[q];
             }
-            P.partials[it] = make_double2(a, b);
+            P.partials[ix] = make_double2(a, b);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
         if (++k == S) { k = 0; phase ^= 1; }
@@ -547,11 +584,14 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
             int kg = 0, ks = 0;
             uint32_t pg = 0, ps = 0;
             int64_t si = first;   // next item whose state is issued
+            int32_t last_b = -1;
             for (int64_t it = first;; it += stride) {
                 const bool more = it < P.item_end;
                 if (more) {
                     mbar_wait(gempty + kg, pg ^ 1);
-                    const Item I = P.items[it];
+                    const int64_t ix = item_at(P, it);
+                    wait_bucket_arrivals(P, ix, last_b);
+                    const Item I = P.items[ix];
                     const uint32_t ng = (uint32_t)I.n_chunk * 8u;
                     mbar_expect_tx(gfull + kg, NR * ng);
 #pragma unroll
@@ -564,7 +604,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
                 }
                 while (si < P.item_end && (!more || si <= it - (int64_t)L * stride)) {
                     mbar_wait(empty + ks, ps ^ 1);
-                    const Item I = P.items[si];
+                    const Item I = P.items[item_at(P, si)];
                     const uint32_t nf = (uint32_t)I.n_chunk * 16u, ng = (uint32_t)I.n_chunk * 8u;
                     mbar_expect_tx(full + ks, 3 * nf + (OWN ? ng : 0));
                     bulk_g2s(st[ks].m, P.m + I.shard_off, nf, full + ks);
@@ -584,7 +624,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
     int kg = 0, ks = 0;
     uint32_t pg = 0, ps = 0;
     for (int64_t it = first; it < P.item_end; it += stride) {
-        const Item I = P.items[it];
+        const int64_t ix = item_at(P, it);
+        const Item I = P.items[ix];
         const GroupConst G = P.groups[I.group];
         mbar_wait(gfull + kg, pg);
         mbar_wait(full + ks, ps);
@@ -621,7 +662,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
                 a += red_w[q];
                 b += red_u[q];
             }
-            P.partials[it] = make_double2(a, b);
+            P.partials[ix] = make_double2(a, b);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
         if (++kg == GS) { kg = 0; pg ^= 1; }

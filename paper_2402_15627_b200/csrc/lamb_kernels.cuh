@@ -85,6 +85,14 @@ struct StepParams {
     int32_t self_src;          // index of this rank's own (local) source in gsrc
     int32_t staged;            // 1: sources j != self_src are shard-ordered staging buffers
                                // (copy-engine schedule): addressed by shard_off, not flat_off
+    // copy-engine schedule, pass A: walk the items in reverse (buckets arrive in backward order)
+    // and wait per bucket until gflags[b * world + j] >= gflag_target for every j != self_src
+    int32_t reverse, world;
+    const int32_t* item_bucket;
+    const uint64_t* gflags;
+    uint64_t gflag_target;
+    int* err;
+    uint64_t timeout_ns;
 };
 
 struct FinalizeParams {

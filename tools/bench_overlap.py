@@ -84,6 +84,7 @@ ev_gath = [torch.cuda.Event() for _ in range(B)]
 ev_ls_done = torch.cuda.Event()
 step = [0]
 last_ce = [0]   # last step done by lamb_step_staged (its params are pushed into the next forward)
+ce_events = []  # per "ce" iteration: forward start / backward start / step start / step end
 
 
 def iteration(mode, comp=comp, ls=ls):
@@ -107,14 +108,20 @@ def iteration(mode, comp=comp, ls=ls):
         ev_ls_done.record(ls)
         comp.wait_event(ev_ls_done)
     elif mode == "ce":
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(comp)
         for b in range(B):
             if last_ce[0]:
                 L.wait_params_bucket(b, last_ce[0], stream=comp)
             gemms(reps_f[b])
+        ev[1].record(comp)
         for b in reversed(range(B)):
             gemms(2 * reps_f[b])
             L.push_grads_bucket(b, t, stream=comp)
+        ev[2].record(comp)
         L.step_staged(t, stream=comp)
+        ev[3].record(comp)
+        ce_events.append(ev)
         last_ce[0] = t
     else:
         for b in range(B):
@@ -154,7 +161,21 @@ for m in ("compute", "serial", "serial_buckets") + (("ce",) if world > 1 else ()
 if world > 1:
     # the first timed "ce" iteration waited on the params of a staged step; re-time after the
     # other modes ran, then the next "ce" run waits on last_ce again (it is still current)
+    ce_events.clear()
     res["ce"] = min(res["ce"], timed("ce"))
+    torch.cuda.synchronize()
+    ph = [[e[i].elapsed_time(e[i + 1]) for i in range(3)] for e in ce_events[a.warmup:]]
+    ce_phases = {k: sum(x[i] for x in ph) / len(ph) for i, k in enumerate(("forward", "backward", "step_staged"))}
+    # the same phases without any transfer in flight (compute mode) for comparison
+    fwd_c = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    fwd_c[0].record(comp)
+    gemms(sum(reps_f))
+    fwd_c[1].record(comp)
+    gemms(2 * sum(reps_f))
+    fwd_c[2].record(comp)
+    torch.cuda.synchronize()
+    ce_phases["forward_compute_only"] = fwd_c[0].elapsed_time(fwd_c[1])
+    ce_phases["backward_compute_only"] = fwd_c[1].elapsed_time(fwd_c[2])
 over = {}
 for c in [int(x) for x in a.ctas.split(",")]:
     L.set_max_ctas(c)
@@ -191,7 +212,8 @@ if rank == 0:
                       "exposed_ms_serial": exposed_serial, "exposed_ms_overlap": exposed_overlap,
                       "hidden_frac": 1.0 - exposed_overlap / exposed_serial if exposed_serial > 0 else None,
                       "ms_ce": res.get("ce"),
-                      "exposed_ms_ce": (res["ce"] - res["compute"]) if "ce" in res else None}))
+                      "exposed_ms_ce": (res["ce"] - res["compute"]) if "ce" in res else None,
+                      "ce_phases_ms_rank0": ce_phases if world > 1 else None}))
 L.close()
 if world > 1:
     dist.barrier()
