@@ -960,8 +960,6 @@ extern "C" lamb_status lamb_step_staged(lamb_t h, int64_t step, void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Plan& p = h->plan;
     const int D = p.world, r = p.rank;
-    // the grad buffer is rewritten by the next backward: this rank's pushes must have read it
-    CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_ce_pushed, 0));
     st = prologue(h, step, s);
     if (st != LAMB_OK) return st;
     h->staged_now = true;
@@ -969,6 +967,9 @@ extern "C" lamb_status lamb_step_staged(lamb_t h, int64_t step, void* stream) {
     h->staged_now = false;
     if (h->t_n < h->t_max) ++h->t_n;
     if (st != LAMB_OK) return st;
+    // the grad buffer is rewritten by the next backward: this rank's pushes must have read it
+    // (joined here, after the update, so the last bucket's push overlaps pass A)
+    CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_ce_pushed, 0));
     // the all-gather on the copy engines, bucket order (the next forward's order)
     CUDA_TRY(h, cudaEventRecord(h->ev_ce_params, s));
     CUDA_TRY(h, cudaStreamWaitEvent(h->ce_stream, h->ev_ce_params, 0));
