@@ -530,3 +530,19 @@ def test_self_check_detects_corruption(lamb):
     assert c["shard_padding_nonzero"] >= 1 and c["flat_padding_nonzero"] >= 1
     assert c["peer_unreachable"] == 0
     L.close()
+
+
+def test_copy_engine_schedule_needs_the_flag(lamb):
+    """lamb_push_grads_bucket / lamb_step_staged / lamb_wait_params_bucket on a handle without
+    LAMB_FLAG_CE (here D = 1) fail with EUNSUPPORTED and leave the handle usable."""
+    wl = W.toy()
+    L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups)
+    L.synth_init(spec_of(wl), wl.seed)
+    for call in (lambda: L.push_grads_bucket(0, 1), lambda: L.step_staged(1), lambda: L.wait_params_bucket(0, 1)):
+        with pytest.raises(lamb.LambError) as ei:
+            call()
+        assert ei.value.status == lamb.LAMB_EUNSUPPORTED
+    L.synth_grads(spec_of(wl), wl.seed, 1, 1)
+    L.step(1)
+    torch.cuda.synchronize()
+    L.close()
