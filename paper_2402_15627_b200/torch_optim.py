@@ -15,6 +15,14 @@ P:689-701); LAMB per PAPER.md §3.1 P:288-293 (update rule and readings: DESIGN.
 
 Parameter groups follow torch.optim conventions ([{"params": [...], "lr": ..., ...}, ...]).
 Parameters must be bf16 CUDA tensors on this rank's device.
+
+`overlap=True` (D > 1) runs the paper's DP overlap (§3.2) on the copy engines
+(DESIGN.md §7b #2b): a post-accumulate-grad hook pushes each bucket's gradients to the peers'
+staging as soon as the backward has produced all of them (`lamb_push_grads_bucket`), `step()`
+runs `lamb_step_staged` (the all-gather then streams into the next forward), and a global
+module forward-pre-hook makes the forward of a module wait for the buckets its own parameters
+live in (`lamb_wait_params_bucket`).  Parameters must therefore be used through `nn.Module`
+forwards; results are bit-identical to `overlap=False`.
 """
 from __future__ import annotations
 
@@ -29,7 +37,8 @@ class LambOptimizer:
     def __init__(self, params: Iterable, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-6,
                  weight_decay: float = 0.0, adapt: bool = True, bias_correction: bool = True,
                  world_size: int = 1, rank: int = 0, pg=None, comm_mode: int = lamb.LAMB_COMM_FUSED,
-                 bucket_cap: int = 0, max_grad_norm: float = 0.0, graph: bool = False):
+                 bucket_cap: int = 0, max_grad_norm: float = 0.0, graph: bool = False,
+                 overlap: bool = False):
         params = list(params)
         if params and not isinstance(params[0], dict):
             params = [{"params": params}]
@@ -54,8 +63,11 @@ class LambOptimizer:
         if not self.params:
             raise ValueError("no parameters")
         self.device = self.params[0].device.index or 0
+        self.overlap = bool(overlap) and world_size > 1
+        if self.overlap and (comm_mode != lamb.LAMB_COMM_FUSED or max_grad_norm > 0):
+            raise ValueError("overlap=True needs comm_mode=FUSED and no global clipping")
         self.L = lamb.Lamb(table, self.groups, world_size=world_size, rank=rank, device=self.device,
-                           comm_mode=comm_mode, bucket_cap=bucket_cap, pg=pg, graph=graph)
+                           comm_mode=comm_mode, bucket_cap=bucket_cap, pg=pg, graph=graph, ce=self.overlap)
         # fp32 master = the current bf16 values (exact), then the params become buffer views
         flat = torch.zeros(self.L.plan.flat_size, dtype=torch.float32, device=f"cuda:{self.device}")
         for p, off in zip(self.params, self.L.plan.tensor_off.tolist()):
@@ -69,6 +81,64 @@ class LambOptimizer:
         if max_grad_norm > 0:
             self.L.set_grad_clip(max_grad_norm)
         self.t = 0
+        self._hooks = []
+        if self.overlap:
+            self._setup_overlap()
+
+    # ---------------- copy-engine overlap (overlap=True)
+    def _setup_overlap(self) -> None:
+        tb = self.L.plan.tensor_bucket.tolist()
+        self._n_buckets = int(self.L.plan.buckets.shape[0])
+        self._bucket_size = [0] * self._n_buckets
+        self._bucket_of = {}
+        for p, b in zip(self.params, tb):
+            self._bucket_size[b] += 1
+            self._bucket_of[id(p)] = b
+        self._pending = list(self._bucket_size)   # params of bucket b still without this step's grad
+        self._pushed = [False] * self._n_buckets
+        self._staged = 0                            # last step done by lamb_step_staged
+        self._awaited = [True] * self._n_buckets    # bucket's params of _staged awaited this forward
+        gv = self.L.grad_views()
+        for p, g in zip(self.params, gv):
+            self._hooks.append(p.register_post_accumulate_grad_hook(self._make_grad_hook(p, g.view(p.shape))))
+        self._hooks.append(torch.nn.modules.module.register_module_forward_pre_hook(self._forward_pre_hook))
+
+    def _make_grad_hook(self, p, gview):
+        b = self._bucket_of[id(p)]
+
+        def hook(param):
+            if param.grad is not None and param.grad.data_ptr() != gview.data_ptr():
+                gview.copy_(param.grad)   # autograd replaced .grad: back into the library buffer
+                param.grad = gview
+            self._pending[b] -= 1
+            if self._pending[b] == 0 and not self._pushed[b]:
+                self.L.push_grads_bucket(b, self.t + 1)
+                self._pushed[b] = True
+        return hook
+
+    def _forward_pre_hook(self, module, args):
+        if not self._staged:
+            return
+        for p in module.parameters(recurse=False):
+            b = self._bucket_of.get(id(p))
+            if b is not None and not self._awaited[b]:
+                self.L.wait_params_bucket(b, self._staged)
+                self._awaited[b] = True
+
+    def wait_params(self) -> None:
+        """Make the current stream wait for every bucket's all-gather (e.g. before using the
+        parameters outside a module forward)."""
+        if self.overlap and self._staged:
+            for b in range(self._n_buckets):
+                if not self._awaited[b]:
+                    self.L.wait_params_bucket(b, self._staged)
+                    self._awaited[b] = True
+
+    def close(self) -> None:
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
+        self.L.close()
 
     @torch.no_grad()
     def zero_grad(self, set_to_none: bool = False) -> None:
@@ -77,6 +147,18 @@ class LambOptimizer:
 
     @torch.no_grad()
     def step(self, closure=None) -> None:
+        if self.overlap:
+            self.wait_params()   # (a forward that skipped some modules)
+            for b in range(self._n_buckets):   # buckets whose params got no gradient this step
+                if not self._pushed[b]:
+                    self.L.push_grads_bucket(b, self.t + 1)
+            self.t += 1
+            self.L.step_staged(self.t)
+            self._staged = self.t
+            self._pending = list(self._bucket_size)
+            self._pushed = [False] * self._n_buckets
+            self._awaited = [False] * self._n_buckets
+            return
         for p, g in zip(self.params, self.L.grad_views()):   # autograd may have replaced .grad
             if p.grad is not None and p.grad.data_ptr() != g.data_ptr():
                 g.view(p.shape).copy_(p.grad)

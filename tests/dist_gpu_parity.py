@@ -455,6 +455,44 @@ def torch_case(world, rank, local, mode):
         print(f"[ok] LambOptimizer DP loop D={world} mode={mode} == oracle on mean grads", flush=True)
 
 
+def torch_overlap_case(world, rank, local, mode):
+    """LambOptimizer(overlap=True): gradient pushes from post-accumulate-grad hooks during the
+    backward, the staged step, per-module waits for the all-gather in the next forward — the
+    parameters after every step are bitwise those of LambOptimizer(overlap=False)."""
+    from paper_2402_15627_b200 import lamb
+    from paper_2402_15627_b200.torch_optim import LambOptimizer
+    if mode != lamb.LAMB_COMM_FUSED:
+        return
+
+    def build():
+        torch.manual_seed(0)
+        return torch.nn.Sequential(torch.nn.Linear(64, 300), torch.nn.GELU(), torch.nn.Linear(300, 200),
+                                   torch.nn.GELU(), torch.nn.Linear(200, 17)).cuda().bfloat16()
+    mA, mB = build(), build()
+    kw = dict(lr=2.0 ** -7, weight_decay=0.01, world_size=world, rank=rank, pg=dist.group.WORLD,
+              comm_mode=mode, bucket_cap=9000)
+    oA, oB = LambOptimizer(mA.parameters(), overlap=True, **kw), LambOptimizer(mB.parameters(), **kw)
+    assert oA.L.plan.buckets.shape[0] > 2
+    torch.manual_seed(1 + rank)
+    for it in range(4):
+        x = torch.randn(32, 64, device="cuda", dtype=torch.bfloat16)
+        for m, o in ((mA, oA), (mB, oB)):
+            o.zero_grad()
+            m(x).float().pow(2).mean().backward()
+            o.step()
+        oA.wait_params()
+        torch.cuda.synchronize()
+        for pa, pb in zip(mA.parameters(), mB.parameters()):
+            assert torch.equal(pa.detach().view(torch.int16), pb.detach().view(torch.int16)), it
+    for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V):
+        assert np.array_equal(oA.L.get_state(k).view(np.uint32), oB.L.get_state(k).view(np.uint32))
+    oA.close()
+    oB.L.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] LambOptimizer(overlap=True) D={world} == overlap=False (bitwise, 4 steps)", flush=True)
+
+
 def failure_case(world, rank, local, mode):
     """Failure detection: (1) a rank passing a different table makes lamb_create fail on every
     rank; (2) in FUSED mode a rank that skips a step makes the others' barriers time out
@@ -571,6 +609,7 @@ def main():
     replicated_case(world, rank, local, mode)
     ce_case(world, rank, local, mode)
     torch_case(world, rank, local, mode)
+    torch_overlap_case(world, rank, local, mode)
     os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"
     failure_case(world, rank, local, mode)
     if a.big:
