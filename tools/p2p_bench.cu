@@ -44,6 +44,24 @@ __global__ void a2a(Ptrs P, int D, int me, size_t bytes_per_peer, char* local) {
 }
 
 template <typename V, bool PUSH>
+__global__ void a2a_s(Ptrs P, int D, int me, size_t bytes_per_peer, size_t nbytes, char* local) {
+    const size_t nv = nbytes / sizeof(V);
+    const int np = D - 1;
+    const int j = (me + 1 + (int)(blockIdx.x % np)) % D;
+    const size_t nb = gridDim.x / np;
+    const size_t b = blockIdx.x / np;
+    for (size_t k = b * blockDim.x + threadIdx.x; k < nv; k += nb * blockDim.x) {
+        if (PUSH) {
+            reinterpret_cast<V*>(P.dst[j] + (size_t)me * bytes_per_peer)[k] =
+                reinterpret_cast<const V*>(local + (size_t)j * bytes_per_peer)[k];
+        } else {
+            reinterpret_cast<V*>(local + (size_t)j * bytes_per_peer)[k] =
+                __ldcs(reinterpret_cast<const V*>(P.src[j] + (size_t)me * bytes_per_peer) + k);
+        }
+    }
+}
+
+template <typename V, bool PUSH>
 float run(int D, size_t bpp, std::vector<char*>& remote, std::vector<char*>& local, int grid) {
     std::vector<cudaEvent_t> e0(D), e1(D);
     for (int g = 0; g < D; ++g) {
@@ -142,6 +160,78 @@ float run_ce(int D, size_t bpp, std::vector<char*>& remote, std::vector<char*>& 
     return (float)(bpp * (D - 1)) / (best * 1e-3f) / 1e9f;
 }
 
+// SM pushes/pulls on the first (1 - ce_frac) of every peer's bytes while the copy engines move
+// the rest, all at once: does the fabric give more than either path alone?
+float run_mixed(int D, size_t bpp, std::vector<char*>& remote, std::vector<char*>& local, int grid, double ce_frac,
+                bool push) {
+    const size_t ce_b = (size_t)(bpp * ce_frac) / 4096 * 4096, sm_b = bpp - ce_b;
+    std::vector<cudaEvent_t> e0(D), e1(D);
+    std::vector<std::vector<cudaStream_t>> st(D);
+    for (int g = 0; g < D; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaEventCreate(&e0[g]));
+        CK(cudaEventCreate(&e1[g]));
+        st[g].resize(D);
+        for (auto& x : st[g]) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    }
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaDeviceSynchronize());
+        }
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaEventRecord(e0[g], 0));
+            Ptrs P;
+            for (int j = 0; j < D; ++j) {
+                P.src[j] = remote[j];
+                P.dst[j] = remote[j];
+            }
+            // SM part: the same a2a kernel over the first sm_b bytes of each peer block (stride bpp)
+            if (sm_b) {
+                CK(cudaStreamWaitEvent(st[g][0], e0[g], 0));
+                if (push) a2a_s<uint4, true><<<grid, 256, 0, st[g][0]>>>(P, D, g, bpp, sm_b, local[g]);
+                else a2a_s<uint4, false><<<grid, 256, 0, st[g][0]>>>(P, D, g, bpp, sm_b, local[g]);
+            }
+            int k = 1;
+            for (int j = 0; j < D && ce_b; ++j) {
+                if (j == g) continue;
+                CK(cudaStreamWaitEvent(st[g][k], e0[g], 0));
+                if (push)
+                    CK(cudaMemcpyPeerAsync(remote[j] + (size_t)g * bpp + sm_b, j, local[g] + (size_t)j * bpp + sm_b, g,
+                                           ce_b, st[g][k]));
+                else
+                    CK(cudaMemcpyPeerAsync(local[g] + (size_t)j * bpp + sm_b, g, remote[j] + (size_t)g * bpp + sm_b, j,
+                                           ce_b, st[g][k]));
+                ++k;
+            }
+            for (auto& x : st[g]) {
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(ev, x));
+                CK(cudaStreamWaitEvent(0, ev, 0));
+                CK(cudaEventDestroy(ev));
+            }
+            CK(cudaEventRecord(e1[g], 0));
+        }
+        float worst = 0;
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaEventSynchronize(e1[g]));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0[g], e1[g]));
+            worst = ms > worst ? ms : worst;
+        }
+        best = worst < best ? worst : best;
+    }
+    for (int g = 0; g < D; ++g) {
+        CK(cudaSetDevice(g));
+        for (auto& x : st[g]) CK(cudaStreamDestroy(x));
+    }
+    return (float)(bpp * (D - 1)) / (best * 1e-3f) / 1e9f;
+}
+
 int main(int argc, char** argv) {
     const int D = argc > 1 ? atoi(argv[1]) : 2;
     const size_t mib = argc > 2 ? (size_t)atoll(argv[2]) : 512;
@@ -175,6 +265,10 @@ int main(int argc, char** argv) {
     for (int split : {1, 4}) {
         printf(", \"ce_push_s%d\": %.1f", split, run_ce(D, bpp, remote, local, true, split));
         printf(", \"ce_pull_s%d\": %.1f", split, run_ce(D, bpp, remote, local, false, split));
+    }
+    for (double f : {0.1, 0.2, 0.3, 0.4}) {
+        printf(", \"mixed_push_ce%.1f\": %.1f", f, run_mixed(D, bpp, remote, local, sms * 6, f, true));
+        printf(", \"mixed_pull_ce%.1f\": %.1f", f, run_mixed(D, bpp, remote, local, sms * 6, f, false));
     }
     printf("}\n");
     return 0;
