@@ -280,12 +280,20 @@ def ce_case(world, rank, local, mode):
         return
     rng = np.random.default_rng(505)
     tensors = W.random_table(rng, 50, max_numel=7000, p_big=0.2, big=50_000) + W.stress_tensors(0, 300)
+    # tiny tensors alone in a bucket: some ranks' slices of those buckets are all padding (no items)
+    tensors += [W.TensorSpec("tiny0", 17, W.NO_DECAY, W.INIT_UNIFORM, W.GEXP_MATRIX),
+                W.TensorSpec("big0", 12_000, W.DECAY, W.INIT_UNIFORM, W.GEXP_MATRIX),
+                W.TensorSpec("tiny1", 3, W.NO_DECAY, W.INIT_UNIFORM, W.GEXP_MATRIX)]
     wl = W.Workload("ce", 79, tensors, W.default_groups(lr=2.0 ** -7))
     spec = spec_of(wl)
     mk = lambda ce: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
                               device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD,
                               bootstrap=BOOT, ce=ce)
     A, B = mk(True), mk(False)
+    segs_per_bucket = np.bincount([int(A.plan.tensor_bucket[i]) for (i, _, _, _) in A.plan.segments.tolist()],
+                                  minlength=A.plan.buckets.shape[0])
+    if rank == world - 1:
+        assert np.any(segs_per_bucket == 0), "want a bucket whose slice on this rank is all padding"
     A.synth_init(spec, wl.seed)
     B.synth_init(spec, wl.seed)
     nb = A.plan.buckets.shape[0]
