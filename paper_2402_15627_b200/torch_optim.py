@@ -87,52 +87,16 @@ class LambOptimizer:
 
     # ---------------- copy-engine overlap (overlap=True)
     def _setup_overlap(self) -> None:
-        tb = self.L.plan.tensor_bucket.tolist()
-        self._n_buckets = int(self.L.plan.buckets.shape[0])
-        self._bucket_size = [0] * self._n_buckets
-        self._bucket_of = {}
-        for p, b in zip(self.params, tb):
-            self._bucket_size[b] += 1
-            self._bucket_of[id(p)] = b
-        self._pending = list(self._bucket_size)   # params of bucket b still without this step's grad
-        self._pushed = [False] * self._n_buckets
-        self._staged = 0                            # last step done by lamb_step_staged
-        self._awaited = [True] * self._n_buckets    # bucket's params of _staged awaited this forward
-        gv = self.L.grad_views()
-        for p, g in zip(self.params, gv):
-            self._hooks.append(p.register_post_accumulate_grad_hook(self._make_grad_hook(p, g.view(p.shape))))
-        self._hooks.append(torch.nn.modules.module.register_module_forward_pre_hook(self._forward_pre_hook))
-
-    def _make_grad_hook(self, p, gview):
-        b = self._bucket_of[id(p)]
-
-        def hook(param):
-            if param.grad is not None and param.grad.data_ptr() != gview.data_ptr():
-                gview.copy_(param.grad)   # autograd replaced .grad: back into the library buffer
-                param.grad = gview
-            self._pending[b] -= 1
-            if self._pending[b] == 0 and not self._pushed[b]:
-                self.L.push_grads_bucket(b, self.t + 1)
-                self._pushed[b] = True
-        return hook
-
-    def _forward_pre_hook(self, module, args):
-        if not self._staged:
-            return
-        for p in module.parameters(recurse=False):
-            b = self._bucket_of.get(id(p))
-            if b is not None and not self._awaited[b]:
-                self.L.wait_params_bucket(b, self._staged)
-                self._awaited[b] = True
+        self._ov = BucketOverlap(self.params, self.L.plan.tensor_bucket.tolist(), int(self.L.plan.buckets.shape[0]),
+                                 push=self.L.push_grads_bucket, wait=self.L.wait_params_bucket,
+                                 grad_views=[g.view(p.shape) for p, g in zip(self.params, self.L.grad_views())])
+        self._hooks = self._ov.install()
 
     def wait_params(self) -> None:
         """Make the current stream wait for every bucket's all-gather (e.g. before using the
         parameters outside a module forward)."""
-        if self.overlap and self._staged:
-            for b in range(self._n_buckets):
-                if not self._awaited[b]:
-                    self.L.wait_params_bucket(b, self._staged)
-                    self._awaited[b] = True
+        if self.overlap:
+            self._ov.wait_all()
 
     def close(self) -> None:
         for h in self._hooks:
@@ -148,16 +112,10 @@ class LambOptimizer:
     @torch.no_grad()
     def step(self, closure=None) -> None:
         if self.overlap:
-            self.wait_params()   # (a forward that skipped some modules)
-            for b in range(self._n_buckets):   # buckets whose params got no gradient this step
-                if not self._pushed[b]:
-                    self.L.push_grads_bucket(b, self.t + 1)
+            self._ov.before_step(self.t + 1)   # pending waits and pushes of this step
             self.t += 1
             self.L.step_staged(self.t)
-            self._staged = self.t
-            self._pending = list(self._bucket_size)
-            self._pushed = [False] * self._n_buckets
-            self._awaited = [False] * self._n_buckets
+            self._ov.after_step(self.t)
             return
         for p, g in zip(self.params, self.L.grad_views()):   # autograd may have replaced .grad
             if p.grad is not None and p.grad.data_ptr() != g.data_ptr():
@@ -176,3 +134,80 @@ class LambOptimizer:
 
     def load_path(self, path: str) -> None:
         self.t = self.L.checkpoint_load(path)
+
+
+class BucketOverlap:
+    """Host bookkeeping of the copy-engine overlap (pure Python; the GPU work is in `push` /
+    `wait`).  Per training step: `push(b, t)` exactly once per bucket, as soon as the backward
+    has accumulated the gradient of the bucket's last parameter (post-accumulate-grad hooks);
+    per forward after a staged step: `wait(b, t_staged)` once per bucket, right before the first
+    module whose own parameters live in bucket b runs (a global module forward-pre-hook).
+    `before_step` pushes buckets whose parameters got no gradient and waits for buckets no
+    module used; `after_step` arms the next forward's waits."""
+
+    def __init__(self, params, bucket_of, n_buckets: int, push, wait, grad_views=None):
+        self.params = list(params)
+        self.n = n_buckets
+        self.push, self.wait = push, wait
+        self.grad_views = grad_views
+        self.size = [0] * n_buckets
+        self.bucket_of = {}
+        for p, b in zip(self.params, bucket_of):
+            self.size[b] += 1
+            self.bucket_of[id(p)] = b
+        self.pending = list(self.size)
+        self.pushed = [False] * n_buckets
+        self.staged = 0
+        self.awaited = [True] * n_buckets
+        self.t_next = 1
+
+    def install(self):
+        hooks = []
+        for i, p in enumerate(self.params):
+            hooks.append(p.register_post_accumulate_grad_hook(self._grad_hook(i)))
+        hooks.append(torch.nn.modules.module.register_module_forward_pre_hook(self._pre_hook))
+        return hooks
+
+    def _grad_hook(self, i):
+        b = self.bucket_of[id(self.params[i])]
+        gview = self.grad_views[i] if self.grad_views is not None else None
+
+        def hook(param):
+            if gview is not None and param.grad is not None and param.grad.data_ptr() != gview.data_ptr():
+                gview.copy_(param.grad)   # autograd replaced .grad: back into the library buffer
+                param.grad = gview
+            self.pending[b] -= 1
+            if self.pending[b] == 0 and not self.pushed[b]:
+                self.push(b, self.t_next)
+                self.pushed[b] = True
+        return hook
+
+    def _pre_hook(self, module, args):
+        if not self.staged:
+            return
+        for p in module.parameters(recurse=False):
+            b = self.bucket_of.get(id(p))
+            if b is not None and not self.awaited[b]:
+                self.wait(b, self.staged)
+                self.awaited[b] = True
+
+    def wait_all(self):
+        if self.staged:
+            for b in range(self.n):
+                if not self.awaited[b]:
+                    self.wait(b, self.staged)
+                    self.awaited[b] = True
+
+    def before_step(self, t: int):
+        self.wait_all()   # (a forward that skipped some modules)
+        for b in range(self.n):   # buckets whose params got no gradient this step
+            if not self.pushed[b]:
+                self.push(b, t)
+                self.pushed[b] = True
+
+    def after_step(self, t: int):
+        self.staged = t
+        self.t_next = t + 1
+        self.pending = list(self.size)
+        self.pushed = [False] * self.n
+        self.awaited = [False] * self.n
