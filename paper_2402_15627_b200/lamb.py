@@ -241,8 +241,12 @@ class Lamb:
             if pg is None:
                 raise ValueError("bootstrap='host' needs a process group")
             ag = _pg_allgather(pg)
-            check(lamb_create_with_allgather(self._tensors, len(numels), garr, len(groups), ctypes.byref(cfg),
-                                             ctypes.cast(ag, _vp), None, ctypes.byref(self.h)))
+            _ag_errors.clear()
+            st = lamb_create_with_allgather(self._tensors, len(numels), garr, len(groups), ctypes.byref(cfg),
+                                            ctypes.cast(ag, _vp), None, ctypes.byref(self.h))
+            if st != LAMB_OK:
+                msg = (lamb_last_error(None) or b"").decode()
+                raise LambError(st, msg + (" (" + "; ".join(_ag_errors) + ")" if _ag_errors else ""))
         else:
             if bootstrap != "nccl":
                 raise ValueError("bootstrap must be 'nccl' or 'host'")
@@ -416,12 +420,17 @@ def _pg_allgather(pg):
             dist.all_gather_object(out, ctypes.string_at(send, nbytes), group=pg)
             for j, b in enumerate(out):
                 if len(b) != nbytes:
+                    _ag_errors.append(f"rank {j} sent {len(b)} bootstrap bytes, expected {nbytes}")
                     return 1
                 ctypes.memmove(recv + j * nbytes, b, nbytes)
             return 0
-        except Exception:
+        except Exception as e:   # no exception may cross the C boundary: report it after the call
+            _ag_errors.append(f"{type(e).__name__}: {e}")
             return 1
     return _ALLGATHER_FN(fn)
+
+
+_ag_errors: List[str] = []   # messages of failed bootstrap all-gathers (appended to the LambError)
 
 
 def broadcast_unique_id(pg, rank: int, device: int) -> bytes:

@@ -68,7 +68,9 @@ def body_host_allgather(rank, world):
     nb2 = 8 + rank
     send2 = (ctypes.c_uint8 * nb2)()
     recv2 = (ctypes.c_uint8 * (nb2 * world))()
+    lamb._ag_errors.clear()
     assert call(ctypes.addressof(send2), ctypes.addressof(recv2), nb2, None) == 1
+    assert lamb._ag_errors and "bootstrap bytes" in lamb._ag_errors[-1]   # reported, not swallowed
 
 
 def body_unique_id(rank, world):
