@@ -280,10 +280,11 @@ static lamb_status bootstrap_allgather(lamb_ctx* h, const void* mine, void* all,
     }
     char* dbuf = nullptr;
     CUDA_TRY(h, cudaMalloc(&dbuf, bytes * (D + 1)));
+    // freed on every return path, the error returns of the TRY macros included
+    std::unique_ptr<char, cudaError_t (*)(void*)> guard(dbuf, cudaFree);
     CUDA_TRY(h, cudaMemcpy(dbuf + bytes * D, mine, bytes, cudaMemcpyHostToDevice));
     NCCL_TRY(h, ncclAllGather(dbuf + bytes * D, dbuf, bytes, ncclChar, h->comm, 0));
     CUDA_TRY(h, cudaMemcpy(all, dbuf, bytes * D, cudaMemcpyDeviceToHost));
-    cudaFree(dbuf);
     return LAMB_OK;
 }
 
@@ -1138,8 +1139,16 @@ extern "C" lamb_status lamb_set_master(lamb_t h, const float* full, int32_t on_d
     }
     const float* src = full;
     float* tmp = nullptr;
+    // the staging copy is freed on every return path; an error return synchronises first so
+    // that no queued copy still reads it (the success path synchronises below)
+    auto release = [s](float* q) {
+        cudaStreamSynchronize(s);
+        cudaFree(q);
+    };
+    std::unique_ptr<float, decltype(release)> guard(nullptr, release);
     if (!on_device) {
         CUDA_TRY(h, dalloc(&tmp, (size_t)p.flat_size));
+        guard.reset(tmp);
         CUDA_TRY(h, cudaMemcpyAsync(tmp, full, (size_t)p.flat_size * 4, cudaMemcpyHostToDevice, s));
         src = tmp;
     }
@@ -1147,7 +1156,6 @@ extern "C" lamb_status lamb_set_master(lamb_t h, const float* full, int32_t on_d
     CUDA_TRY(h, cudaMemsetAsync(h->m, 0, (size_t)p.shard_size * 4, s));
     CUDA_TRY(h, cudaMemsetAsync(h->v, 0, (size_t)p.shard_size * 4, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
-    if (tmp) cudaFree(tmp);
     h->master_set = true;
     return LAMB_OK;
 }
@@ -1426,9 +1434,9 @@ extern "C" lamb_status lamb_synth_philox(const uint32_t ctr[4], const uint32_t k
     uint32_t in[6] = {ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1]};
     uint32_t* d = nullptr;
     CUDA_TRY(nullptr, cudaMalloc(&d, 10 * sizeof(uint32_t)));
+    std::unique_ptr<uint32_t, cudaError_t (*)(void*)> guard(d, cudaFree);   // freed on every path
     CUDA_TRY(nullptr, cudaMemcpy(d, in, sizeof(in), cudaMemcpyHostToDevice));
     CUDA_TRY(nullptr, synth_philox(d, d + 6));
     CUDA_TRY(nullptr, cudaMemcpy(out, d + 6, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    cudaFree(d);
     return LAMB_OK;
 }
