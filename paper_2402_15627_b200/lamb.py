@@ -324,14 +324,20 @@ class Lamb:
         check(lamb_wait_params_bucket(self.h, int(bucket), int(t), self._stream(stream)), self.h)
 
     def step_host(self, host_grads, host_params, t: int, stream=None) -> None:
+        """host_grads / host_params: contiguous 2-byte CPU tensors (bf16 or int16 bit patterns)
+        of flat_size elements, pinned for the copies to overlap."""
+        n = self.plan.flat_size
+        _check_flat(host_grads, n, _BF16_LIKE, "host_grads", cuda=False)
+        _check_flat(host_params, n, _BF16_LIKE, "host_params", cuda=False)
         check(lamb_step_host(self.h, ctypes.c_void_p(host_grads.data_ptr()),
                              ctypes.c_void_p(host_params.data_ptr()), int(t), self._stream(stream)), self.h)
 
     # -- state
     def set_master(self, full_flat, stream=None) -> None:
         """full_flat: torch fp32 tensor (CPU or CUDA) of flat_size elements."""
+        _check_flat(full_flat, self.plan.flat_size, ("torch.float32",), "full_flat",
+                    cuda=None, device=self.device)
         on_dev = 1 if full_flat.is_cuda else 0
-        full_flat = full_flat.contiguous()
         check(lamb_set_master(self.h, ctypes.c_void_p(full_flat.data_ptr()), on_dev, self._stream(stream)), self.h)
 
     def synth_init(self, spec: Sequence[tuple], seed: int, stream=None) -> None:
@@ -404,6 +410,26 @@ class Lamb:
             self.close()
         except Exception:
             pass
+
+
+_BF16_LIKE = ("torch.bfloat16", "torch.int16", "torch.uint16")
+
+
+def _check_flat(t, n: int, dtypes: Sequence[str], name: str, cuda: Optional[bool] = None,
+                device: Optional[int] = None) -> None:
+    """Validate a buffer handed to the library by pointer: the C side reads exactly n elements
+    of the documented dtype from its first byte, so a wrong size, dtype, layout or device would
+    be an out-of-bounds or garbage read, not an error."""
+    if str(t.dtype) not in dtypes:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected one of {', '.join(dtypes)}")
+    if t.numel() != n:
+        raise ValueError(f"{name}: {t.numel()} elements, expected flat_size = {n}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if cuda is not None and bool(t.is_cuda) != cuda:
+        raise ValueError(f"{name} must be a {'CUDA' if cuda else 'CPU'} tensor")
+    if device is not None and t.is_cuda and t.device.index != device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the handle on cuda:{device}")
 
 
 _ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)

@@ -57,6 +57,25 @@ def test_errors_without_gpu_are_reported(L):
         L.host_plan([5], 2, 2)
 
 
+def test_binding_rejects_mis_sized_host_buffers(L):
+    # the C side reads flat_size elements from the pointer it is given: the binding checks
+    # size, dtype and layout before handing a tensor over
+    import torch
+    n = 1024
+    L._check_flat(torch.zeros(n, dtype=torch.bfloat16), n, L._BF16_LIKE, "g", cuda=False)
+    L._check_flat(torch.zeros(n, dtype=torch.int16), n, L._BF16_LIKE, "g", cuda=False)
+    with pytest.raises(ValueError, match="elements"):
+        L._check_flat(torch.zeros(n - 8, dtype=torch.bfloat16), n, L._BF16_LIKE, "g")
+    with pytest.raises(ValueError, match="dtype"):
+        L._check_flat(torch.zeros(n, dtype=torch.float32), n, L._BF16_LIKE, "g")
+    with pytest.raises(ValueError, match="dtype"):
+        L._check_flat(torch.zeros(n, dtype=torch.float64), n, ("torch.float32",), "w")
+    with pytest.raises(ValueError, match="contiguous"):
+        L._check_flat(torch.zeros(2 * n, dtype=torch.bfloat16)[::2], n, L._BF16_LIKE, "g")
+    with pytest.raises(ValueError, match="CUDA"):
+        L._check_flat(torch.zeros(n, dtype=torch.bfloat16), n, L._BF16_LIKE, "g", cuda=True)
+
+
 def compare(L, numels, D, cap):
     op = oracle.plan(numels, D, cap)
     for r in range(D):
