@@ -302,7 +302,8 @@ lamb_status lamb_get_step_info(lamb_t h, lamb_step_info* out);
  * may continue.  A second save first waits for the previous one.
  * EINVAL: null path.  ESTATE: master not set.  ENOMEM: staging allocation. */
 lamb_status lamb_checkpoint_save(lamb_t h, const char* path, int64_t step, void* stream);
-/* Waits for the background write of the last save; EINVAL with the I/O error if it failed. */
+/* Waits for the background write of the last save; EINVAL with the I/O error if it failed
+ * (reported once: the next save or load starts clean). */
 lamb_status lamb_checkpoint_wait(lamb_t h);
 /* COLLECTIVE.  Reads only this rank's segments of W, M, V from `path` (saved at any world
  * size), uploads them, rebuilds the bf16 param buffer (own slices cast, then all-gathered),

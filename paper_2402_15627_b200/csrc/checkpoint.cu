@@ -131,7 +131,12 @@ lamb_status ensure_stage(lamb_ctx* h) {
 extern "C" lamb_status lamb_checkpoint_wait(lamb_t h) {
     if (!h) return lamb_fail(nullptr, LAMB_EINVAL, "null handle");
     if (h->ck_thread.joinable()) h->ck_thread.join();
-    if (h->ck_status != LAMB_OK) return lamb_fail(h, h->ck_status, h->ck_error);
+    if (h->ck_status != LAMB_OK) {
+        // reported once: a failed save must not block every later save or load
+        const lamb_status st = h->ck_status;
+        h->ck_status = LAMB_OK;
+        return lamb_fail(h, st, h->ck_error);
+    }
     return LAMB_OK;
 }
 
@@ -178,17 +183,20 @@ extern "C" lamb_status lamb_checkpoint_save(lamb_t h, const char* path, int64_t 
             memcpy(hdr.data() + sizeof(H), p.numel.data(), 8 * (size_t)T);
             // never truncate below data written by other ranks: size the file exactly
             if (ftruncate(fd, doff + 3 * N * 4) != 0 || !pwrite_all(fd, hdr.data(), hdr.size(), 0)) {
+                fail_io("header");   // before close(), which may overwrite errno
                 close(fd);
-                return fail_io("header");
+                return;
             }
         }
         if (!run_io(fd, segment_tasks(p, h->ck_stage, cum, doff), true)) {
+            fail_io("write");   // before close(), which may overwrite errno
             close(fd);
-            return fail_io("write");
+            return;
         }
         if (fdatasync(fd) != 0) {
+            fail_io("fdatasync");   // before close(), which may overwrite errno
             close(fd);
-            return fail_io("fdatasync");
+            return;
         }
         close(fd);
     });

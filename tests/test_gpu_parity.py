@@ -287,6 +287,14 @@ def test_checkpoint_resume_and_reshard(lamb, tmp_path):
     with pytest.raises(lamb.LambError):   # a different parameter table is refused
         C = lamb.Lamb([(10, 0)], wl.groups)
         C.checkpoint_load(path)
+    # a failed background write is reported once by the next wait, then a save works again
+    A.checkpoint_save(str(tmp_path / "no_such_dir" / "x.ckpt"), 5)
+    with pytest.raises(lamb.LambError, match="open"):
+        A.checkpoint_wait()
+    A.checkpoint_wait()
+    A.checkpoint_save(str(tmp_path / "again.ckpt"), 5)
+    A.checkpoint_wait()
+    assert read_checkpoint(str(tmp_path / "again.ckpt"))["step"] == 5
     A.close()
 
 
