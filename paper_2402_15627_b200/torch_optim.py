@@ -78,6 +78,7 @@ class LambOptimizer:
         for p, v, g in zip(self.params, pv, gv):
             p.data = v.view(p.shape)
             p.grad = g.view(p.shape)
+        self._gviews = [p.grad for p in self.params]   # cached: step() compares pointers only
         if max_grad_norm > 0:
             self.L.set_grad_clip(max_grad_norm)
         self.t = 0
@@ -117,10 +118,10 @@ class LambOptimizer:
             self.L.step_staged(self.t)
             self._ov.after_step(self.t)
             return
-        for p, g in zip(self.params, self.L.grad_views()):   # autograd may have replaced .grad
+        for p, g in zip(self.params, self._gviews):   # autograd may have replaced .grad
             if p.grad is not None and p.grad.data_ptr() != g.data_ptr():
-                g.view(p.shape).copy_(p.grad)
-                p.grad = g.view(p.shape)
+                g.copy_(p.grad)
+                p.grad = g
         self.t += 1
         self.L.step(self.t)
 
