@@ -1,5 +1,5 @@
-"""Soak test (test infrastructure: it calls oracle/, so it lives under tests/): many consecutive LAMB steps through the C-ABI.  Checks that the step time does
-not drift (§6.3 P:991 reports MFU decaying over a long run from skewed collective
+"""Soak test: many consecutive LAMB steps through the C-ABI (test infrastructure: it calls
+oracle/, so it lives under tests/).  Checks that the step time does not drift (§6.3 P:991 reports MFU decaying over a long run from skewed collective
 launches) and that after many steps the small tensors still match the oracle (barrier epochs,
 events, graph replay and the bias-correction constants stay consistent).
 
