@@ -21,6 +21,7 @@
 // coalesced ld/st.global.cs, several chunks per lane in flight, profiles/r01_final.md) remain
 // as LAMB_TUNE variants and serve the NCCL-mode fp32 input.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -1230,37 +1231,40 @@ static cudaError_t pass_a_pf(const StepParams& p, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// Dynamic shared memory above 48 KB must be opted into per kernel AND per device (the attribute
+// lives in the device's context): a process may drive handles on several GPUs, so the opt-in is
+// recorded per device, not once per process.
+static void set_smem_once(std::atomic<uint64_t>& done, const void* kernel, size_t smem) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    done.fetch_or(bit, std::memory_order_acq_rel);
+}
+
 template <int NS, int U, int PD>
 static cudaError_t pass_a_ring(const StepParams& p, int grid, cudaStream_t s) {
     const size_t smem = (size_t)(kThreads / 32) * PD * U * NS * 32 * sizeof(uint2);
-    static bool attr = [&] {
-        cudaFuncSetAttribute(pass_a_ring_kernel<NS, U, PD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return true;
-    }();
-    (void)attr;
+    static std::atomic<uint64_t> attr{0};
+    set_smem_once(attr, (const void*)pass_a_ring_kernel<NS, U, PD>, smem);
     pass_a_ring_kernel<NS, U, PD><<<grid, kThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 // one CTA per SM (the ring uses ~170 KB of shared memory); `grid` (the SM budget) caps it
 static int tma_grid(int grid) {
-    static const int sms = [] {
-        int dev = 0, n = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n;
-    }();
+    int dev = 0, sms = 0;   // the current device's SM count (cached by the runtime)
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return grid < sms ? grid : sms;
 }
 
 template <int NS>
 static cudaError_t pass_a_tma(const StepParams& p, int grid, cudaStream_t s) {
     const size_t smem = sizeof(TmaStage<NS>) * tma_stages_a<NS>() + 2 * tma_stages_a<NS>() * sizeof(uint64_t);
-    static const bool attr = [&] {
-        cudaFuncSetAttribute(pass_a_tma_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return true;
-    }();
-    (void)attr;
+    static std::atomic<uint64_t> attr{0};
+    set_smem_once(attr, (const void*)pass_a_tma_kernel<NS>, smem);
     pass_a_tma_kernel<NS><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
     return cudaGetLastError();
 }
@@ -1270,11 +1274,8 @@ static cudaError_t pass_a_tma2(const StepParams& p, int grid, cudaStream_t s) {
     constexpr int NR = OWN ? NS - 1 : NS;
     constexpr int GS = tma2_grad_stages<NS, SS, OWN>();
     const size_t smem = sizeof(TmaStateStage<OWN>) * SS + sizeof(TmaGradStage<NR>) * GS + 2 * (SS + GS) * sizeof(uint64_t);
-    static const bool attr = [&] {
-        cudaFuncSetAttribute(pass_a_tma2_kernel<NS, SS, OWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return true;
-    }();
-    (void)attr;
+    static std::atomic<uint64_t> attr{0};
+    set_smem_once(attr, (const void*)pass_a_tma2_kernel<NS, SS, OWN>, smem);
     pass_a_tma2_kernel<NS, SS, OWN><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
     return cudaGetLastError();
 }
@@ -1355,11 +1356,8 @@ template <int ND, bool BULK>
 static cudaError_t pass_b_tma(const StepParams& p, int grid, cudaStream_t s) {
     const size_t smem = sizeof(TmaStageB) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t) + 64 +
                         (BULK ? sizeof(TmaParamStage) * kTmaStages : 0);
-    static const bool attr = [&] {
-        cudaFuncSetAttribute(pass_b_tma_kernel<ND, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return true;
-    }();
-    (void)attr;
+    static std::atomic<uint64_t> attr{0};
+    set_smem_once(attr, (const void*)pass_b_tma_kernel<ND, BULK>, smem);
     pass_b_tma_kernel<ND, BULK><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
     return cudaGetLastError();
 }

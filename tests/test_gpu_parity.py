@@ -90,6 +90,29 @@ def test_group_variants(lamb):
     L.close()
 
 
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_two_devices_in_one_process(lamb):
+    """Handles on two GPUs in one process (lamb.h: several handles per process): the
+    shared-memory opt-in of the TMA passes is per device, so the second device's launches run
+    too, and both devices give bitwise-identical results on the same inputs."""
+    rng = np.random.default_rng(78)
+    wl = W.Workload("two", 41, W.random_table(rng, 20, max_numel=30000), W.default_groups())
+    outs = []
+    for dev in (0, 1):
+        L = run_gpu(wl, steps=2, cap=50_000, device=dev)
+        outs.append([L.get_state(k) for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V)]
+                    + [L.param_buffer().view(torch.int16).cpu().numpy()])
+        L.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+    orc = oracle.OracleRun(wl)
+    for t in (1, 2):
+        orc.step(t)
+    L = run_gpu(wl, steps=2, cap=50_000, device=1)
+    compare_state(L, orc, 2)
+    L.close()
+
+
 def test_determinism_bitwise(lamb):
     """H13: two runs give bitwise-identical w, m, v, params (no float atomics)."""
     rng = np.random.default_rng(77)
