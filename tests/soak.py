@@ -1,7 +1,8 @@
 """Soak test: many consecutive LAMB steps through the C-ABI (test infrastructure: it calls
-oracle/, so it lives under tests/).  Checks that the step time does not drift (§6.3 P:991 reports MFU decaying over a long run from skewed collective
-launches) and that after many steps the small tensors still match the oracle (barrier epochs,
-events, graph replay and the bias-correction constants stay consistent).
+oracle/, so it lives under tests/).  Checks that the step time does not drift (§6.3
+P:991 reports MFU decaying over a long run from skewed collective launches) and that after
+many steps the small tensors still match the oracle (barrier epochs, events, graph replay and
+the bias-correction constants stay consistent).
 
     python tests/soak.py --steps 2000 [--graph]
     python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tests/soak.py
