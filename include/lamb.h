@@ -18,7 +18,8 @@
  *     cudaStream_t passed as void* (NULL = legacy default stream).
  *   - Collective calls (marked COLLECTIVE) must be made by all world_size ranks with
  *     identical tensor/group tables, config (except rank/device) and step.
- *   - One handle is not thread-safe; several handles per process are allowed.
+ *   - One handle is not thread-safe; several handles per process are allowed, on the same or
+ *     on different devices (tests/test_gpu_parity.py::test_two_devices_in_one_process).
  *   - There is no CPU fallback: a device that is not sm_100 gives LAMB_EUNSUPPORTED.
  */
 #ifndef LAMB_H_
