@@ -105,3 +105,16 @@ def test_planner_bit_exact_random(L, seed):
     cap = int(rng.choice([0, 1, 64, 1000, 8192, 30000]))
     for D in range(1, 9):
         compare(L, numels, D, cap if cap else 40_000_000)
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    # no CPU fallback: a copy of the binding next to no liblamb.so refuses to import
+    import importlib.util
+    import shutil
+    src = os.path.join(ROOT, "paper_2402_15627_b200", "lamb.py")
+    dst = tmp_path / "lamb_copy.py"
+    shutil.copy(src, dst)
+    spec = importlib.util.spec_from_file_location("lamb_copy", dst)
+    mod = importlib.util.module_from_spec(spec)
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        spec.loader.exec_module(mod)
