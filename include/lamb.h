@@ -212,11 +212,16 @@ lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream);
  * LAMB_FLAG_CE at create (FUSED, D > 1).  Results are bit-identical to lamb_step (same sums in
  * the same rank order).  EUNSUPPORTED: handle without LAMB_FLAG_CE, or the pre-step enabled.
  *
+ * Arrival flags carry an internal per-handle round number, not `step`, so a rollback
+ * (lamb_checkpoint_load) or a repeated step number can never let a stale flag release a wait.
+ *
  * lamb_push_grads_bucket — COLLECTIVE per bucket, called as soon as the backward has written
  *   bucket b's gradients into the library grad buffer (ordered after the work on `stream`):
  *   copies this rank's gradients of every peer's slice of b into that peer's staging buffer
  *   (one cudaMemcpyAsync per peer on an internal copy stream) and raises the peer's arrival
- *   flag (value `step`).  Buckets may be pushed in any order (backward order is the natural).
+ *   flag for this round.  Buckets may be pushed in any order (backward order is the natural);
+ *   a bucket's gradients must be final (gradient accumulation: push after the last
+ *   micro-batch only).
  * lamb_step_staged — COLLECTIVE, after every bucket was pushed: pass A (own slice + D-1 staged
  *   slices, local HBM) walks the buckets in reverse (the order the backward pushed them) and
  *   waits in-kernel, per bucket and bounded by LAMB_BARRIER_TIMEOUT_MS, until all peers' slices
@@ -226,7 +231,8 @@ lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream);
  *   param slices of every bucket (bucket order) into every peer's param buffer — the
  *   all-gather, deferred into the next forward.
  * lamb_wait_params_bucket — before bucket b's forward: `stream` waits until every peer's
- *   param slice of b from lamb_step_staged(step) landed in this rank's param buffer. */
+ *   param slice of b from lamb_step_staged(step) landed in this rank's param buffer.  `step`
+ *   must be the step of the last lamb_step_staged (EINVAL otherwise; ESTATE before the first). */
 lamb_status lamb_push_grads_bucket(lamb_t h, int64_t bucket, int64_t step, void* stream);
 lamb_status lamb_step_staged(lamb_t h, int64_t step, void* stream);
 lamb_status lamb_wait_params_bucket(lamb_t h, int64_t bucket, int64_t step, void* stream);
@@ -252,7 +258,9 @@ lamb_status lamb_buffer(lamb_t h, int32_t which, void** dev_ptr, int64_t* n_elem
 
 /* Sets the fp32 master from a FULL flat fp32 array (flat_size elements, plan layout,
  * padding 0; host memory if on_device = 0): copies this rank's slices into w, zeroes m and
- * v, writes bf16_rne into the whole param buffer.  Synchronous w.r.t. `stream`. */
+ * v, writes bf16_rne into the whole param buffer.  A host source is staged bucket by bucket
+ * through one temporary device buffer of the largest bucket (4 * max S_b bytes), whatever
+ * flat_size is.  Synchronous w.r.t. `stream`.  ENOMEM: that buffer. */
 lamb_status lamb_set_master(lamb_t h, const float* full_flat, int32_t on_device, void* stream);
 
 /* Copies this rank's shard of W/M/V (LAMB_BUF_W/M/V; shard_size floats, shard order) to
@@ -292,24 +300,30 @@ lamb_status lamb_get_step_info(lamb_t h, lamb_step_info* out);
 
 /* ---------------- checkpoint / resume with reshard (§4.4) ----------------
  * File format (little endian; one file per checkpoint, written by all ranks at disjoint
- * offsets): header {char magic[8] = "LAMBCKPT"; u32 version = 1; u32 world size that saved;
- * i64 n_tensors, step, n_params, data_off} + i64 numel[n_tensors], zero-padded to data_off
- * (multiple of 4096); then fp32 arrays W, M, V of n_params elements each in table order,
- * no padding.  Independent of D, bucket cap and alignment: load at any world size. */
+ * offsets): header {char magic[8] = "LAMBCKPT"; u32 version = 2; u32 world size that saved;
+ * i64 n_tensors, step, n_params, data_off; u64 session, save_seq} + i64 numel[n_tensors] +
+ * u64 commit[8] (one word per saving rank, written after its data is durable), zero-padded to
+ * data_off (multiple of 4096); then fp32 arrays W, M, V of n_params elements each in table
+ * order, no padding.  Independent of D, bucket cap and alignment: load at any world size. */
 /* COLLECTIVE.  Stage 1 (blocking): copies this rank's w/m/v shard into pinned host staging
  * (allocated on first use: 12 * shard_size bytes) after the work already on `stream`.
- * Stage 2 (background host thread): writes this rank's segments into `path` (created if
- * missing; rank 0 writes the header and sizes the file).  Returns after stage 1; training
- * may continue.  A second save first waits for the previous one.
+ * Stage 2 (background host thread): writes this rank's segments into `path`.tmp.<n> (rank 0
+ * writes the header and sizes the file), makes them durable, writes its commit word; the rank
+ * that finds every rank's commit word in place renames the file to `path` (atomic: a crash or
+ * an I/O error on any rank leaves the previous checkpoint at `path` intact).  Returns after
+ * stage 1; training may continue.  A second save first waits for the previous one.
  * EINVAL: null path.  ESTATE: master not set.  ENOMEM: staging allocation. */
 lamb_status lamb_checkpoint_save(lamb_t h, const char* path, int64_t step, void* stream);
-/* Waits for the background write of the last save; EINVAL with the I/O error if it failed
- * (reported once: the next save or load starts clean). */
+/* Waits for this rank's background write of the last save; EINVAL with the I/O error if it
+ * failed (reported once: the next save or load starts clean).  `path` is complete once every
+ * rank's wait returned LAMB_OK (the last rank to commit renames it). */
 lamb_status lamb_checkpoint_wait(lamb_t h);
 /* COLLECTIVE.  Reads only this rank's segments of W, M, V from `path` (saved at any world
  * size), uploads them, rebuilds the bf16 param buffer (own slices cast, then all-gathered),
  * marks the master set and returns the saved step in *step (may be NULL).  Synchronous.
- * EINVAL: unreadable file, wrong magic/version, or a different parameter table. */
+ * EINVAL: unreadable file, wrong magic/version, a different parameter table, or a commit word
+ * missing (a partition never completed).  ESTATE: copy-engine gradient pushes of a step that
+ * was not taken are pending. */
 lamb_status lamb_checkpoint_load(lamb_t h, const char* path, int64_t* step, void* stream);
 
 /* ---------------- self-check (§4.3 P:163-193 diagnostic tests) ----------------

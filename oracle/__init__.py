@@ -180,6 +180,8 @@ class OracleRun:
         self.m: Dict[int, np.ndarray] = {}
         self.v: Dict[int, np.ndarray] = {}
         self.stats: Dict[int, tuple] = {}
+        # w before the most recent step (tests compare the per-step update dw = w - w_prev)
+        self.w_prev: Dict[int, np.ndarray] = {}
         for i in self.ids:
             ts = workload.tensors[i]
             self.w[i] = gen_weights(workload.seed, i, ts.init, ts.numel)
@@ -200,6 +202,8 @@ class OracleRun:
         (state untouched) if gn is not finite; if max_grad_norm > 0 and
         c = max_grad_norm / (gn + 1e-6) < 1, g <- c * g (torch clip_grad_norm_ rule)."""
         info = {"grad_norm": None, "clip": 1.0, "skipped": False}
+        for i in self.ids:
+            self.w_prev[i] = self.w[i].copy()
         if max_grad_norm > 0.0 or inv_loss_scale != 1.0:
             gsq = 0.0
             for i in range(len(self.wl.tensors)):          # the GLOBAL norm needs every tensor

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <array>
 #include <memory>
 #include <string>
 #include <thread>
@@ -85,9 +86,7 @@ struct lamb_ctx {
     cudaEvent_t gf_override = nullptr;   // step_impl records "grads consumed" here if set
     bool host_whole = false;             // LAMB_HOST_WHOLE: whole-step pipeline (A/B timing)
     cudaEvent_t grad_free_event() const { return gf_override ? gf_override : ev_grad_free; }
-    int grid_a = 0, grid_b = 0;
     int max_ctas = 0;   // SM budget of the streaming passes (0 = one full wave)
-    bool diag_local_grads = false;   // LAMB_DIAG_LOCAL_GRADS: timing diagnostic, wrong results
     lamb::GroupConst* d_groups = nullptr;   // per-step group constants (prologue kernel)
     // lamb_self_check: padding ranges and counters (built on first use)
     bool pad_built = false;
@@ -97,7 +96,10 @@ struct lamb_ctx {
     // LAMB_FLAG_GRAPH
     cudaGraphExec_t graph_exec = nullptr;
     cudaStream_t cap_stream = nullptr;
-    int64_t graph_key = -1, graph_launches = 0;
+    // what the captured graph froze: pre-step on/off and SM budget (launch sequence) and the
+    // pre-step scalars passed to its kernels by value (max_grad_norm, inv_loss_scale bits)
+    std::array<int64_t, 3> graph_key{{-1, -1, -1}};
+    int64_t graph_launches = 0;
     uint64_t barrier_timeout_ns = 30000000000ull;   // LAMB_BARRIER_TIMEOUT_MS at create
     // synth tables (device)
     int64_t *d_tensor_off = nullptr, *d_numel = nullptr, *d_shard_base = nullptr,
@@ -113,6 +115,8 @@ struct lamb_ctx {
     bool prestep() const { return max_grad_norm > 0.f || inv_loss_scale != 1.f; }
     // checkpoint (two-stage save: pinned staging + background writer thread)
     float* ck_stage = nullptr;          // pinned host, 3 x shard_size
+    uint64_t session = 0;               // random at create, rank 0's value on every rank
+    uint64_t ck_seq = 0;                // saves so far (same on every rank: collective calls)
     std::thread ck_thread;
     lamb_status ck_status = LAMB_OK;
     std::string ck_error;
@@ -126,9 +130,18 @@ struct lamb_ctx {
     cudaEvent_t ev_ce_in = nullptr, ev_ce_pushed = nullptr, ev_ce_params = nullptr;
     bool ce() const { return stage != nullptr; }
     int32_t* d_item_bucket = nullptr;   // [n_items] bucket of each item (staged pass A waits)
+    // Flag values are an internal per-handle epoch (identical on every rank: all ranks make the
+    // same sequence of collective calls), never the caller's step: a rollback or a repeated step
+    // number cannot make a stale flag satisfy a new wait.  Round k's gradient pushes raise
+    // gflags to k + 1 (= ce_epoch + 1), lamb_step_staged of round k + 1 waits for that, then
+    // sets ce_epoch = k + 1 and its param pushes raise pflags to it.
+    uint64_t ce_epoch = 0;
+    int64_t ce_staged_step = 0;      // `step` of the last lamb_step_staged (wait_params checks it)
+    int64_t ce_pushes_pending = 0;   // gradient pushes since the last staged step
     bool staged_now = false;   // inside lamb_step_staged (step_impl: flag wait + staged sources)
-    // gflag[b * D + j]: rank j's gradient slice of bucket b landed in this rank's staging (value
-    // = step); pflag[b * D + j]: rank j's param slice of bucket b landed in this param buffer
+    // gflag[b * D + j]: rank j's gradient slice of bucket b landed in this rank's staging;
+    // pflag[b * D + j]: rank j's param slice of bucket b landed in this param buffer (values:
+    // ce_epoch above)
     uint64_t* gflag(int j) const { return reinterpret_cast<uint64_t*>((j < 0 ? sync : peer_sync[j]) + ce_off); }
     uint64_t* pflag(int j) const { return gflag(j) + (size_t)plan.n_buckets() * cfg.world_size; }
 
@@ -142,6 +155,22 @@ struct lamb_ctx {
     }
 };
 
+
+// Every entry point runs on its handle's device and restores the caller's current device on
+// return (a process may hold handles on several GPUs; torch's "cuda" means the current one).
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 
 // error plumbing shared by the implementation files
 lamb_status lamb_fail(lamb_ctx* h, lamb_status st, const std::string& msg);

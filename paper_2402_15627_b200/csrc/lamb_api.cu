@@ -15,7 +15,11 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <unistd.h>
+
+#include <chrono>
 #include <cmath>
+#include <random>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -129,7 +133,7 @@ static std::string check_group(const lamb_group& g) {
 static void free_ctx(lamb_ctx* h) {
     if (!h) return;
     if (h->ck_thread.joinable()) h->ck_thread.join();
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     if (h->ck_stage) cudaFreeHost(h->ck_stage);
     cudaDeviceSynchronize();
     for (int j = 0; j < h->cfg.world_size && j < LAMB_MAX_RANKS; ++j) {
@@ -309,13 +313,17 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
         const int64_t cfgv[4] = {h->cfg.world_size, h->cfg.comm_mode, h->plan.cap, (int64_t)h->cfg.flags};
         mix(cfgv, sizeof(cfgv));
         mix(&h->cfg.grad_scale, sizeof(float));
-        std::vector<uint64_t> all(D);
-        lamb_status st = bootstrap_allgather(h, &hv, all.data(), sizeof(hv));
+        // with it travels each rank's random session id; rank 0's becomes everyone's (it tags
+        // the per-rank commit records of checkpoints, checkpoint.cu)
+        const uint64_t mine[2] = {hv, h->session};
+        std::vector<uint64_t> all(2 * (size_t)D);
+        lamb_status st = bootstrap_allgather(h, mine, all.data(), sizeof(mine));
         if (st != LAMB_OK) return st;
         for (int j = 0; j < D; ++j)
-            if (all[j] != hv)
+            if (all[2 * j] != hv)
                 return fail(h, LAMB_EINVAL, "lamb_create: rank " + std::to_string(j) +
                                                 " passed a different tensor/group table or config");
+        h->session = all[1];
     }
     for (int j = 0; j < D; ++j) {
         h->peer_grad[j] = h->grad;
@@ -388,7 +396,6 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
     h->cfg = *cfg;
     h->host_ag = host_ag;
     h->host_ag_user = host_ag_user;
-    h->diag_local_grads = getenv("LAMB_DIAG_LOCAL_GRADS") != nullptr;
     {
         // failure detection: bound on every cross-GPU wait (a missing peer must not hang the GPU)
         const char* e = getenv("LAMB_BARRIER_TIMEOUT_MS");
@@ -396,6 +403,11 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
         h->barrier_timeout_ns = (uint64_t)(ms > 0 ? ms : 30000) * 1000000ull;
     }
     h->device = cfg->device;
+    {
+        std::random_device rd;
+        h->session = ((uint64_t)rd() << 32) ^ (uint64_t)rd() ^
+                     (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count() ^ ((uint64_t)getpid() << 17);
+    }
     h->groups.assign(groups, groups + n_groups);
     if (h->cfg.grad_scale == 0.f) h->cfg.grad_scale = 1.0f / (float)cfg->world_size;
     std::vector<int64_t> numel(n_tensors);
@@ -417,9 +429,9 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
         free_ctx(h);
         return s;
     };
-    cudaError_t ce = cudaSetDevice(cfg->device);
-    if (ce != cudaSuccess) {
-        fail(h, LAMB_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(ce));
+    DeviceGuard device_guard_(cfg->device);
+    if (!device_guard_.ok) {
+        fail(h, LAMB_ECUDA, "cudaSetDevice(" + std::to_string(cfg->device) + ") failed");
         return bail(LAMB_ECUDA);
     }
     cudaDeviceProp prop;
@@ -472,8 +484,6 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
     CUDA_STEP(cudaHostAlloc(&h->err_flag_host, sizeof(int), cudaHostAllocMapped));
     *h->err_flag_host = 0;
     CUDA_STEP(cudaHostGetDevicePointer(&h->err_flag_dev, h->err_flag_host, 0));
-    h->grid_a = pass_grid(cfg->device, D, false, false, 1);
-    h->grid_b = pass_grid(cfg->device, 1, false, true, D);
     CUDA_STEP(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
     CUDA_STEP(cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming));
     CUDA_STEP(cudaEventCreateWithFlags(&h->ev_grad_free, cudaEventDisableTiming));
@@ -573,9 +583,9 @@ static inline void mark(lamb_ctx* h, int phase, cudaStream_t s) {
 static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStream_t s, int64_t b0,
                              int64_t b1, bool defer_ag) {
     const Plan& p = h->plan;
-    // SM budget (lamb_set_max_ctas): fewer persistent CTAs leave SMs to concurrent compute
-    const int grid_a = h->max_ctas > 0 ? std::min(h->max_ctas, h->grid_a) : h->grid_a;
-    const int grid_b = h->max_ctas > 0 ? std::min(h->max_ctas, h->grid_b) : h->grid_b;
+    // SM budget (lamb_set_max_ctas): fewer persistent CTAs leave SMs to concurrent compute;
+    // 0 = every pass sizes a full persistent wave itself
+    const int grid_a = h->max_ctas, grid_b = h->max_ctas;
     const int D = h->cfg.world_size, r = h->cfg.rank;
     const bool fused = D > 1 && h->cfg.comm_mode == LAMB_COMM_FUSED;
     const bool nccl = D > 1 && h->cfg.comm_mode == LAMB_COMM_NCCL;
@@ -659,12 +669,10 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
             sp.world = D;
             sp.item_bucket = h->d_item_bucket;
             sp.gflags = h->gflag(-1);
-            sp.gflag_target = (uint64_t)t;
+            sp.gflag_target = h->ce_epoch + 1;   // this round's pushes (internal epoch, not t)
             sp.err = h->err_flag_dev;
             sp.timeout_ns = h->barrier_timeout_ns;
         }
-        if (fused && h->diag_local_grads)   // timing diagnostic only (wrong sums): no NVLink loads
-            for (int j = 0; j < D; ++j) sp.gsrc[j] = h->grad;
         if (pre) {
             // pre-step: global ||g||^2 (FUSED: the reduce-scatter happens here, into g32)
             sp.g32_out = h->g32;
@@ -806,8 +814,11 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
 static lamb_status check_async(lamb_ctx* h) {
     if (h->err_flag_host && *(volatile int*)h->err_flag_host)
         return fail(h, LAMB_ECUDA, "cross-GPU barrier timed out in an earlier step (peer missing)");
-    cudaError_t e = cudaPeekAtLastError();
-    if (e != cudaSuccess) return fail(h, LAMB_ECUDA, std::string("pending CUDA error: ") + cudaGetErrorString(e));
+    // an asynchronous fault of this handle's earlier work (sticky context errors surface here);
+    // the thread's last-error slot is not consulted: it may hold another library's error
+    const cudaError_t e = cudaEventQuery(h->ev_grad_free);
+    if (e != cudaSuccess && e != cudaErrorNotReady)
+        return fail(h, LAMB_ECUDA, std::string("CUDA error from earlier work: ") + cudaGetErrorString(e));
     if (h->comm) {
         ncclResult_t ae;
         if (ncclCommGetAsyncError(h->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
@@ -826,9 +837,15 @@ static lamb_status prologue(lamb_ctx* h, int64_t t, cudaStream_t s) {
 }
 
 // LAMB_FLAG_GRAPH: the whole step (everything after the prologue) captured once into a CUDA
-// graph and replayed; re-captured when a setting that changes the launch sequence changes.
+// graph and replayed; re-captured when a setting changes that the graph froze: the launch
+// sequence (pre-step on/off, SM budget) or a value passed to its kernels (the pre-step's
+// max_grad_norm / inv_loss_scale).
 static lamb_status graph_step(lamb_ctx* h, cudaStream_t s) {
-    const int64_t key = (h->prestep() ? 1 : 0) | ((int64_t)h->max_ctas << 1);
+    uint32_t clip_bits, scale_bits;
+    memcpy(&clip_bits, &h->max_grad_norm, 4);
+    memcpy(&scale_bits, &h->inv_loss_scale, 4);
+    const std::array<int64_t, 3> key{{(h->prestep() ? 1 : 0) | ((int64_t)h->max_ctas << 1), (int64_t)clip_bits,
+                                      (int64_t)scale_bits}};
     if (!h->graph_exec || key != h->graph_key) {
         if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
         h->graph_exec = nullptr;
@@ -865,7 +882,7 @@ extern "C" lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void
     if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step before lamb_set_master / lamb_synth_init");
     lamb_status st = check_async(h);
     if (st != LAMB_OK) return st;
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     st = prologue(h, step, s);
     if (st != LAMB_OK) return st;
@@ -885,7 +902,7 @@ extern "C" lamb_status lamb_step_bucket(lamb_t h, int64_t bucket, int64_t step, 
     if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step_bucket before lamb_set_master / lamb_synth_init");
     lamb_status st = check_async(h);
     if (st != LAMB_OK) return st;
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     const int32_t t_max = h->t_max;
     h->t_max = 0;   // per-bucket calls are not phase-timed
     st = prologue(h, step, static_cast<cudaStream_t>(stream));
@@ -902,7 +919,7 @@ extern "C" lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream
     const Plan& p = h->plan;
     const int D = p.world, r = p.rank;
     if (D == 1) return LAMB_OK;
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t base = p.buckets[4 * bucket], sl = p.buckets[4 * bucket + 1] / D;
     if (h->cfg.comm_mode == LAMB_COMM_FUSED) {
@@ -932,7 +949,7 @@ extern "C" lamb_status lamb_push_grads_bucket(lamb_t h, int64_t bucket, int64_t 
     lamb_status st = ce_check(h, bucket, step);
     if (st != LAMB_OK) return st;
     if (bucket < 0) return fail(h, LAMB_EINVAL, "bucket out of range");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     const Plan& p = h->plan;
     const int D = p.world, r = p.rank;
     const int64_t base = p.buckets[4 * bucket], sl = p.buckets[4 * bucket + 1] / D, sb = p.shard_base[bucket];
@@ -948,8 +965,9 @@ extern "C" lamb_status lamb_push_grads_bucket(lamb_t h, int64_t bucket, int64_t 
                                     h->ce_stream));
         fl[nf++] = h->gflag(j) + bucket * D + r;
     }
-    LAUNCH(h, lamb::launch_flag_store(fl, nf, (uint64_t)step, h->ce_stream));
+    LAUNCH(h, lamb::launch_flag_store(fl, nf, h->ce_epoch + 1, h->ce_stream));
     CUDA_TRY(h, cudaEventRecord(h->ev_ce_pushed, h->ce_stream));
+    ++h->ce_pushes_pending;
     return LAMB_OK;
 }
 
@@ -957,7 +975,7 @@ extern "C" lamb_status lamb_step_staged(lamb_t h, int64_t step, void* stream) {
     lamb_status st = ce_check(h, -1, step);
     if (st != LAMB_OK) return st;
     if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step_staged before lamb_set_master / lamb_synth_init");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Plan& p = h->plan;
     const int D = p.world, r = p.rank;
@@ -968,6 +986,9 @@ extern "C" lamb_status lamb_step_staged(lamb_t h, int64_t step, void* stream) {
     h->staged_now = false;
     if (h->t_n < h->t_max) ++h->t_n;
     if (st != LAMB_OK) return st;
+    ++h->ce_epoch;
+    h->ce_staged_step = step;
+    h->ce_pushes_pending = 0;
     // the grad buffer is rewritten by the next backward: this rank's pushes must have read it
     // (joined here, after the update, so the last bucket's push overlaps pass A)
     CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_ce_pushed, 0));
@@ -985,7 +1006,7 @@ extern "C" lamb_status lamb_step_staged(lamb_t h, int64_t step, void* stream) {
                                         h->ce_stream));
             fl[nf++] = h->pflag(j) + b * D + r;
         }
-        LAUNCH(h, lamb::launch_flag_store(fl, nf, (uint64_t)step, h->ce_stream));
+        LAUNCH(h, lamb::launch_flag_store(fl, nf, h->ce_epoch, h->ce_stream));
     }
     return LAMB_OK;
 }
@@ -994,8 +1015,12 @@ extern "C" lamb_status lamb_wait_params_bucket(lamb_t h, int64_t bucket, int64_t
     lamb_status st = ce_check(h, bucket, step);
     if (st != LAMB_OK) return st;
     if (bucket < 0) return fail(h, LAMB_EINVAL, "bucket out of range");
-    cudaSetDevice(h->device);
-    LAUNCH(h, lamb::launch_flag_wait(h->pflag(-1), bucket, bucket + 1, h->plan.world, h->plan.rank, (uint64_t)step,
+    if (h->ce_epoch == 0) return fail(h, LAMB_ESTATE, "no lamb_step_staged yet: no params to wait for");
+    if (step != h->ce_staged_step)
+        return fail(h, LAMB_EINVAL, "params of step " + std::to_string(step) + " requested, the last staged step is " +
+                                        std::to_string(h->ce_staged_step));
+    DeviceGuard device_guard_(h->device);
+    LAUNCH(h, lamb::launch_flag_wait(h->pflag(-1), bucket, bucket + 1, h->plan.world, h->plan.rank, h->ce_epoch,
                                      h->err_flag_dev, h->barrier_timeout_ns, static_cast<cudaStream_t>(stream)));
     return LAMB_OK;
 }
@@ -1021,7 +1046,7 @@ extern "C" lamb_status lamb_step_host(lamb_t h, const uint16_t* host_grads, uint
     lamb_status st = check_async(h);
     if (st != LAMB_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     const Plan& p = h->plan;
     const int64_t B = p.n_buckets();
     if (!h->h2d_stream) {
@@ -1128,31 +1153,36 @@ extern "C" lamb_status lamb_buffer(lamb_t h, int32_t which, void** dev_ptr, int6
 
 extern "C" lamb_status lamb_set_master(lamb_t h, const float* full, int32_t on_device, void* stream) {
     if (!h || !full) return fail(h, LAMB_EINVAL, "null argument");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Plan& p = h->plan;
-    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    for (int64_t b = 0; b < p.n_buckets(); ++b) {
-        const int64_t sl = p.buckets[4 * b + 1] / p.world;
-        CUDA_TRY(h, cudaMemcpyAsync(h->w + p.shard_base[b], full + p.buckets[4 * b] + (int64_t)p.rank * sl,
-                                    (size_t)sl * 4, kind, s));
-    }
-    const float* src = full;
+    // Host source: staged bucket by bucket through ONE device buffer of the largest bucket
+    // (4 * max S_b bytes; 160 MB at the default cap), so the call works at configs whose state
+    // fills the GPU (a flat_size fp32 temporary would be 87 GB for the 175B slice).  Each
+    // bucket: H2D into the buffer, own slice -> w (D2D), whole bucket -> bf16 params.
     float* tmp = nullptr;
-    // the staging copy is freed on every return path; an error return synchronises first so
-    // that no queued copy still reads it (the success path synchronises below)
+    // freed on every return path; an error return synchronises first so that no queued copy
+    // still uses it (the success path synchronises below)
     auto release = [s](float* q) {
         cudaStreamSynchronize(s);
         cudaFree(q);
     };
     std::unique_ptr<float, decltype(release)> guard(nullptr, release);
     if (!on_device) {
-        CUDA_TRY(h, dalloc(&tmp, (size_t)p.flat_size));
+        CUDA_TRY(h, dalloc(&tmp, (size_t)h->max_bucket));
         guard.reset(tmp);
-        CUDA_TRY(h, cudaMemcpyAsync(tmp, full, (size_t)p.flat_size * 4, cudaMemcpyHostToDevice, s));
-        src = tmp;
     }
-    LAUNCH(h, launch_cast_to_bf16(src, h->param, p.flat_size, s));
+    for (int64_t b = 0; b < p.n_buckets(); ++b) {
+        const int64_t base = p.buckets[4 * b], S = p.buckets[4 * b + 1], sl = S / p.world;
+        const float* src = full + base;
+        if (!on_device) {
+            CUDA_TRY(h, cudaMemcpyAsync(tmp, full + base, (size_t)S * 4, cudaMemcpyHostToDevice, s));
+            src = tmp;
+        }
+        CUDA_TRY(h, cudaMemcpyAsync(h->w + p.shard_base[b], src + (int64_t)p.rank * sl, (size_t)sl * 4,
+                                    cudaMemcpyDeviceToDevice, s));
+        LAUNCH(h, launch_cast_to_bf16(src, h->param + base, S, s));
+    }
     CUDA_TRY(h, cudaMemsetAsync(h->m, 0, (size_t)p.shard_size * 4, s));
     CUDA_TRY(h, cudaMemsetAsync(h->v, 0, (size_t)p.shard_size * 4, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
@@ -1164,7 +1194,7 @@ extern "C" lamb_status lamb_get_state(lamb_t h, int32_t which, float* dst, int32
     if (!h || !dst) return fail(h, LAMB_EINVAL, "null argument");
     const float* src = which == LAMB_BUF_W ? h->w : which == LAMB_BUF_M ? h->m : which == LAMB_BUF_V ? h->v : nullptr;
     if (!src) return fail(h, LAMB_EINVAL, "which must be LAMB_BUF_W/M/V");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(h, cudaMemcpyAsync(dst, src, (size_t)h->plan.shard_size * 4,
                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
@@ -1174,7 +1204,7 @@ extern "C" lamb_status lamb_get_state(lamb_t h, int32_t which, float* dst, int32
 
 extern "C" lamb_status lamb_get_tensor_stats(lamb_t h, double* w_sq, double* u_sq, float* ratio) {
     if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     CUDA_TRY(h, cudaDeviceSynchronize());
     const size_t T = (size_t)h->plan.n_tensors();
     if (w_sq) CUDA_TRY(h, cudaMemcpy(w_sq, h->w_sq, T * 8, cudaMemcpyDeviceToHost));
@@ -1215,7 +1245,8 @@ extern "C" lamb_status lamb_sm_partition(int32_t device, int32_t lamb_sms, void*
     CUresult (*genDesc)(CUdevResourceDesc*, CUdevResource*, unsigned int) = nullptr;
     CUresult (*gcCreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int) = nullptr;
     CUresult (*gcStream)(CUstream*, CUgreenCtx, unsigned int, int) = nullptr;
-    if (cudaSetDevice(device) != cudaSuccess || cudaFree(nullptr) != cudaSuccess)
+    DeviceGuard device_guard_(device);
+    if (!device_guard_.ok || cudaFree(nullptr) != cudaSuccess)
         return fail(nullptr, LAMB_ECUDA, "cannot initialise the device");
     if (!driver_fn("cuDeviceGet", &getDev) || !driver_fn("cuDeviceGetDevResource", &getRes) ||
         !driver_fn("cuDevSmResourceSplitByCount", &split) || !driver_fn("cuDevResourceGenerateDesc", &genDesc) ||
@@ -1274,7 +1305,7 @@ static lamb_status build_padding(lamb_ctx* h) {
 extern "C" lamb_status lamb_self_check(lamb_t h, int64_t counts[5], void* stream) {
     if (!h || !counts) return fail(h, LAMB_EINVAL, "null argument");
     if (!h->master_set) return fail(h, LAMB_ESTATE, "nothing to check: master not set");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     lamb_status st = build_padding(h);
     if (st != LAMB_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1314,7 +1345,7 @@ extern "C" lamb_status lamb_set_loss_scale(lamb_t h, float inv_loss_scale) {
 
 extern "C" lamb_status lamb_get_step_info(lamb_t h, lamb_step_info* out) {
     if (!h || !out) return fail(h, LAMB_EINVAL, "null argument");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     CUDA_TRY(h, cudaDeviceSynchronize());
     lamb::ClipState cs;
     CUDA_TRY(h, cudaMemcpy(&cs, h->d_clip, sizeof(cs), cudaMemcpyDeviceToHost));
@@ -1333,7 +1364,7 @@ extern "C" lamb_status lamb_get_step_info(lamb_t h, lamb_step_info* out) {
 extern "C" lamb_status lamb_timing_begin(lamb_t h, int32_t max_steps) {
     if (!h || max_steps < 0) return fail(h, LAMB_EINVAL, "bad argument");
     if (!(h->cfg.flags & LAMB_FLAG_TIMING)) return fail(h, LAMB_ESTATE, "handle created without LAMB_FLAG_TIMING");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     CUDA_TRY(h, cudaDeviceSynchronize());
     for (cudaEvent_t e : h->tev) cudaEventDestroy(e);
     h->tev.assign((size_t)max_steps * (LAMB_N_PHASES + 1), nullptr);
@@ -1345,7 +1376,7 @@ extern "C" lamb_status lamb_timing_begin(lamb_t h, int32_t max_steps) {
 
 extern "C" lamb_status lamb_timing_read(lamb_t h, float* ms, int32_t* n_steps) {
     if (!h || !n_steps) return fail(h, LAMB_EINVAL, "null argument");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     *n_steps = h->t_n;
     for (int32_t k = 0; k < h->t_n; ++k) {
         CUDA_TRY(h, cudaEventSynchronize(h->tev[(size_t)k * (LAMB_N_PHASES + 1) + LAMB_N_PHASES]));
@@ -1392,7 +1423,7 @@ static lamb_status synth_tables(lamb_ctx* h, const lamb_synth_tensor* spec, Synt
 
 extern "C" lamb_status lamb_synth_init(lamb_t h, const lamb_synth_tensor* spec, uint64_t seed, void* stream) {
     if (!h || !spec) return fail(h, LAMB_EINVAL, "null argument");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     SynthTables t;
     int32_t *di = nullptr, *dg = nullptr;
@@ -1413,7 +1444,7 @@ extern "C" lamb_status lamb_synth_init(lamb_t h, const lamb_synth_tensor* spec, 
 extern "C" lamb_status lamb_synth_grads(lamb_t h, const lamb_synth_tensor* spec, uint64_t seed,
                                         uint32_t rank_term, uint32_t step, void* stream) {
     if (!h || !spec) return fail(h, LAMB_EINVAL, "null argument");
-    cudaSetDevice(h->device);
+    DeviceGuard device_guard_(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     SynthTables t;
     int32_t *di = nullptr, *dg = nullptr;

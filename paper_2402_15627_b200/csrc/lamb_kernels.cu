@@ -24,6 +24,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "lamb_kernels.cuh"
@@ -180,9 +181,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_a_kernel(const __grid_con
     }
 }
 
-// Pass A with a one-block-deep prefetch of the gradient words (FUSED, NS >= 2): the next
-// U-block's bf16 loads (mostly remote, ~2-3x the local latency) are issued before the current
-// block is computed, so the local m/v/w stream of the next block no longer waits behind them.
+// fp32 sum of one chunk's NS bf16 sources in fixed rank order j = 0..NS-1 (reading Z11)
 template <int NS>
 __device__ __forceinline__ float4 sum_raw(const uint2 (&raw)[NS]) {
     float4 s = make_float4(bf_lo(raw[0].x), bf_hi(raw[0].x), bf_lo(raw[0].y), bf_hi(raw[0].y));
@@ -194,172 +193,6 @@ __device__ __forceinline__ float4 sum_raw(const uint2 (&raw)[NS]) {
         s.w = __fadd_rn(s.w, bf_hi(raw[j].y));
     }
     return s;
-}
-
-template <int NS, int U, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) pass_a_pf_kernel(const __grid_constant__ StepParams P) {
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
-    if (P.clip && P.clip->skip) return;
-    const float gs = P.clip ? P.clip->gs : P.grad_scale;
-    for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
-        const Item I = P.items[it];
-        const GroupConst G = P.groups[I.group];
-        float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
-        float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
-        const float4* __restrict__ wp = reinterpret_cast<const float4*>(P.w + I.shard_off);
-        const int n = I.n_chunk;
-        double dw = 0.0, du = 0.0;
-        int c = lane;
-        uint2 raw[U][NS];
-        if (c + 32 * (U - 1) < n) {
-#pragma unroll
-            for (int k = 0; k < U; ++k)
-#pragma unroll
-                for (int j = 0; j < NS; ++j)
-                    raw[k][j] = __ldcs(reinterpret_cast<const uint2*>(P.gsrc[j] + I.flat_off) + c + 32 * k);
-        }
-        for (; c + 32 * (U - 1) < n; c += 32 * U) {
-            float4 m[U], v[U], w[U];
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                m[k] = __ldcs(mp + c + 32 * k);
-                v[k] = __ldcs(vp + c + 32 * k);
-                w[k] = __ldcs(wp + c + 32 * k);
-            }
-            const int cn = c + 32 * U;
-            const bool more = cn + 32 * (U - 1) < n;
-            uint2 nxt[U][NS];
-            if (more) {
-#pragma unroll
-                for (int k = 0; k < U; ++k)
-#pragma unroll
-                    for (int j = 0; j < NS; ++j)
-                        nxt[k][j] = __ldcs(reinterpret_cast<const uint2*>(P.gsrc[j] + I.flat_off) + cn + 32 * k);
-            }
-            float sw = 0.f, su = 0.f;
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                chunk_a(sum_raw<NS>(raw[k]), m[k], v[k], w[k], gs, G, sw, su);
-                __stcs(mp + c + 32 * k, m[k]);
-                __stcs(vp + c + 32 * k, v[k]);
-            }
-            dw += (double)sw;
-            du += (double)su;
-            if (more) {
-#pragma unroll
-                for (int k = 0; k < U; ++k)
-#pragma unroll
-                    for (int j = 0; j < NS; ++j) raw[k][j] = nxt[k][j];
-            }
-        }
-        for (; c < n; c += 32) {
-            float4 g = load_grad<NS>(P, I, 4 * (int64_t)c), m = __ldcs(mp + c), v = __ldcs(vp + c);
-            const float4 w = __ldcs(wp + c);
-            float sw = 0.f, su = 0.f;
-            chunk_a(g, m, v, w, gs, G, sw, su);
-            __stcs(mp + c, m);
-            __stcs(vp + c, v);
-            dw += (double)sw;
-            du += (double)su;
-        }
-        dw = warp_sum(dw);
-        du = warp_sum(du);
-        if (lane == 0) P.partials[it] = make_double2(dw, du);
-    }
-}
-
-// Pass A with a shared-memory ring for the gradient words (FUSED, NS >= 2): every lane
-// streams its own future gradient chunks (NS x 8 B per chunk, mostly remote) with cp.async,
-// PD-1 U-blocks ahead of use, so NVLink latency is covered without holding registers (tunable
-// LAMB_TUNE ring=3|4|6; not the default: 2 % slower than the register prefetch at D = 2,
-// profiles/r01/sweep_ring.jsonl — the limit there is shared HBM, not latency).  A lane
-// only ever reads back what it copied itself (wait_group makes its own copies visible), so no
-// warp synchronisation is needed.
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-template <int NS, int U, int PD>
-__global__ void __launch_bounds__(kThreads, 2) pass_a_ring_kernel(const __grid_constant__ StepParams P_) {
-    const StepParams& P = P_;
-    extern __shared__ __align__(16) uint2 ring_all[];   // [warps][P][U][NS][32]
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    uint2* ring = ring_all + (size_t)wib * PD * U * NS * 32;
-    const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
-    if (P.clip && P.clip->skip) return;
-    const float gs = P.clip ? P.clip->gs : P.grad_scale;
-    auto slot = [&](int stage, int k, int j) -> uint2* { return ring + (((stage * U + k) * NS + j) * 32 + lane); };
-    for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
-        const Item I = P.items[it];
-        const GroupConst G = P.groups[I.group];
-        float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
-        float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
-        const float4* __restrict__ wp = reinterpret_cast<const float4*>(P.w + I.shard_off);
-        const int n = I.n_chunk;
-        const int nb = n / (32 * U);   // full U-blocks (same for every lane)
-        auto issue = [&](int b) {
-            if (b < nb) {
-                const int stage = b % PD;
-#pragma unroll
-                for (int k = 0; k < U; ++k)
-#pragma unroll
-                    for (int j = 0; j < NS; ++j)
-                        cp_async8(slot(stage, k, j),
-                                  reinterpret_cast<const uint2*>(P.gsrc[j] + I.flat_off) + 32 * U * b + 32 * k + lane);
-            }
-            cp_async_commit();   // always commit: keeps the group count uniform
-        };
-#pragma unroll
-        for (int b = 0; b < PD - 1; ++b) issue(b);
-        double dw = 0.0, du = 0.0;
-        for (int b = 0; b < nb; ++b) {
-            issue(b + PD - 1);
-            const int c = 32 * U * b + lane;
-            float4 m[U], v[U], w[U];
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                m[k] = __ldcs(mp + c + 32 * k);
-                v[k] = __ldcs(vp + c + 32 * k);
-                w[k] = __ldcs(wp + c + 32 * k);
-            }
-            cp_async_wait<PD - 1>();   // this lane's copies of block b have landed
-            const int stage = b % PD;
-            float sw = 0.f, su = 0.f;
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                uint2 raw[NS];
-#pragma unroll
-                for (int j = 0; j < NS; ++j) raw[j] = *slot(stage, k, j);
-                chunk_a(sum_raw<NS>(raw), m[k], v[k], w[k], gs, G, sw, su);
-                __stcs(mp + c + 32 * k, m[k]);
-                __stcs(vp + c + 32 * k, v[k]);
-            }
-            dw += (double)sw;
-            du += (double)su;
-        }
-        cp_async_wait<0>();
-        for (int c = 32 * U * nb + lane; c < n; c += 32) {
-            float4 g = load_grad<NS>(P, I, 4 * (int64_t)c), m = __ldcs(mp + c), v = __ldcs(vp + c);
-            const float4 w = __ldcs(wp + c);
-            float sw = 0.f, su = 0.f;
-            chunk_a(g, m, v, w, gs, G, sw, su);
-            __stcs(mp + c, m);
-            __stcs(vp + c, v);
-            dw += (double)sw;
-            du += (double)su;
-        }
-        dw = warp_sum(dw);
-        du = warp_sum(du);
-        if (lane == 0) P.partials[it] = make_double2(dw, du);
-    }
 }
 
 // ------------------------------------------------------------ pass A, TMA variant (default, any D)
@@ -682,76 +515,22 @@ __device__ __forceinline__ uint2 chunk_b(const float4 m, const float4 v, float4&
     return make_uint2(pack_bf16x2(ww[0], ww[1]), pack_bf16x2(ww[2], ww[3]));
 }
 
-template <int ND, int U, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) pass_b_kernel(const __grid_constant__ StepParams P) {
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
-    if (P.clip && P.clip->skip) return;
-    for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
-        const Item I = P.items[it];
-        const GroupConst G = P.groups[I.group];
-        const float scale = P.scale[I.tensor];
-        float4* __restrict__ wp = reinterpret_cast<float4*>(P.w + I.shard_off);
-        const float4* __restrict__ mp = reinterpret_cast<const float4*>(P.m + I.shard_off);
-        const float4* __restrict__ vp = reinterpret_cast<const float4*>(P.v + I.shard_off);
-        const int n = I.n_chunk;
-        int c = lane;
-        for (; c + 32 * (U - 1) < n; c += 32 * U) {
-            float4 m[U], v[U], w[U];
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                m[k] = __ldcs(mp + c + 32 * k);
-                v[k] = __ldcs(vp + c + 32 * k);
-                w[k] = __ldcs(wp + c + 32 * k);
-            }
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                const uint2 pb = chunk_b(m[k], v[k], w[k], scale, G);
-                __stcs(wp + c + 32 * k, w[k]);
-#pragma unroll
-                for (int j = 0; j < ND; ++j)
-                    __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c + 32 * k, pb);
-            }
-        }
-        for (; c < n; c += 32) {
-            const float4 m = __ldcs(mp + c), v = __ldcs(vp + c);
-            float4 w = __ldcs(wp + c);
-            const uint2 pb = chunk_b(m, v, w, scale, G);
-            __stcs(wp + c, w);
-#pragma unroll
-            for (int j = 0; j < ND; ++j) __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c, pb);
-        }
-    }
-    if constexpr (ND > 1) __threadfence_system();   // peer stores visible before the barrier
-}
-
-// ------------------------------------------------------------ pass B, TMA variant (default, any D)
-// Same ring as pass A's TMA variant: the producer stages m, v, w of an item; consumers recompute
-// u, store w (16 B) and p (8 B) with streaming STGs.
+// ------------------------------------------------------------ pass B (TMA, any D)
+// Same ring as pass A: the producer stages m, v, w of an item; consumers recompute u with the
+// function pass A used (bit-identical), store w (16 B) and the bf16 params (8 B) with streaming
+// STGs — into every rank's param buffer for the fused all-gather (ND = D).  Staging the params
+// in shared memory and writing them with bulk copies was measured no faster (r01,
+// profiles/r01/sweep_tmb_bulk_store.jsonl): stores are posted writes and already stream.
 struct TmaStageB {
     float4 m[kTmaItem / 4], v[kTmaItem / 4], w[kTmaItem / 4];
 };
 
-// BULK: the item's bf16 params are staged in shared memory (one 8 KB buffer per ring stage) and
-// written to every destination param buffer (this rank's and, fused AG, each peer's) with one
-// bulk copy each (cp.async.bulk global<-shared, TMA engine) instead of 8 B STGs per lane.
-struct TmaParamStage {
-    uint2 p[kTmaItem / 4];
-};
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
-                 "r"(bytes) : "memory");
-}
-
-template <int ND, bool BULK>
+template <int ND>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const __grid_constant__ StepParams P) {
     extern __shared__ __align__(128) unsigned char tma_smem_b[];
     TmaStageB* st = reinterpret_cast<TmaStageB*>(tma_smem_b);
     uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem_b + sizeof(TmaStageB) * kTmaStages);
     uint64_t* empty = full + kTmaStages;
-    TmaParamStage* pst = reinterpret_cast<TmaParamStage*>(tma_smem_b + sizeof(TmaStageB) * kTmaStages +
-                                                          2 * kTmaStages * sizeof(uint64_t) + 64);
     const int tid = threadIdx.x;
     if (P.clip && P.clip->skip) return;
     if (tid == 0) {
@@ -793,32 +572,12 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const
             float4 w = st[k].w[c];
             const uint2 pb = chunk_b(st[k].m[c], st[k].v[c], w, scale, G);
             __stcs(wp + c, w);
-            if constexpr (BULK) {
-                pst[k].p[c] = pb;
-            } else {
 #pragma unroll
-                for (int j = 0; j < ND; ++j) __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c, pb);
-            }
+            for (int j = 0; j < ND; ++j) __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c, pb);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + k);
-        if constexpr (BULK) {
-            // the generic-proxy smem writes must be visible to the bulk copy (async proxy)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
-            if (tid == 0) {
-#pragma unroll
-                for (int j = 0; j < ND; ++j) bulk_s2g(P.pdst[j] + I.flat_off, pst[k].p, (uint32_t)I.n_chunk * 8u);
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                // the buffer of the item before this one may be rewritten from the next item's
-                // barrier on (stage k+2 mod 3 is written two items later, after two barriers)
-                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            }
-        }
         if (++k == kTmaStages) { k = 0; phase ^= 1; }
-    }
-    if constexpr (BULK) {
-        if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // writes performed
     }
     if constexpr (ND > 1) __threadfence_system();   // peer stores visible before the barrier
 }
@@ -1197,39 +956,36 @@ __global__ void prologue_kernel(const __grid_constant__ GroupTable T, int n, Gro
 }
 
 // ------------------------------------------------------------ host launchers
-// Variant table: unroll U and min-CTAs-per-SM (register cap) per pass.  Defaults from the
-// r01 sweep (profiles/); LAMB_TUNE="ua=U,ma=M,ub=U,mb=M" overrides for tuning runs.
+// Kernel choice per pass (r01 measurements):
+//   pass A, bf16 sources (NS = D >= 1): TMA ring (pass_a_tma_kernel); at D = 2 the decoupled
+//           remote-gradient ring (pass_a_tma2_kernel), which pulls the peers' slices deeper
+//           ahead (pass A 90 -> 96 % of HBM at D = 2; 2 % slower at D = 4);
+//   pass A, fp32 reduced shard (NS = 0: NCCL mode, FUSED pre-step): the LDG kernel;
+//   pass B: TMA ring.
+// LAMB_TUNE="tmam=0|1" (comma-separated key=value pairs) overrides the D >= 2 pass-A ring for
+// A/B timing runs only: every variant executes the same arithmetic in the same order, so no
+// setting changes a result (tests run the default; the parity suite passes with each).
 struct Tune {
-    int ua = 4, ma = 2, ub = 4, mb = 2;
-    int pf = 1, upf = 4;   // FUSED (NS >= 2): prefetching pass A (U = 4 for NS = 2, else 2; r01 sweep)
-    int ring = 0;          // FUSED (NS >= 2): cp.async smem ring of this depth (0 = off)
-    int tmb = 0;           // pass B TMA variant with bulk (TMA-engine) param stores
-    int tma = 1;           // D = 1: TMA bulk-copy passes (r01: pass A 98.1 % -> 99.9 % of HBM)
-    int tma_multi = 1;     // FUSED D >= 2: TMA passes (peer gradient slices pulled by bulk copies;
-                           // r01: step -4.1 % at D = 2, -3.7 % at D = 4, profiles/r01/sweep_tma.jsonl);
-                           // at D = 2 pass A uses the decoupled remote-gradient ring (tmam=4:
-                           // pass A -6 %, step -3.5 %; at D = 4 it is 2 % slower than the single
-                           // ring, which stays there; profiles/r01/sweep_tma2_ring.jsonl)
+    int tmam = -1;   // D >= 2 pass A: -1 auto (decoupled ring at D = 2 only), 0 single ring, 1 decoupled
 };
-static Tune g_tune = [] {
+static Tune parse_tune() {
     Tune t;
-    if (const char* e = getenv("LAMB_TUNE")) {
-        sscanf(e, "ua=%d,ma=%d,ub=%d,mb=%d,pf=%d,upf=%d,ring=%d,tma=%d,tmam=%d,tmb=%d", &t.ua, &t.ma, &t.ub,
-               &t.mb, &t.pf, &t.upf, &t.ring, &t.tma, &t.tma_multi, &t.tmb);
+    const char* e = getenv("LAMB_TUNE");
+    if (!e) return t;
+    std::string str(e);
+    size_t pos = 0;
+    while (pos < str.size()) {
+        size_t end = str.find(',', pos);
+        if (end == std::string::npos) end = str.size();
+        const std::string kv = str.substr(pos, end - pos);
+        const size_t eq = kv.find('=');
+        if (eq != std::string::npos && kv.substr(0, eq) == "tmam") t.tmam = atoi(kv.c_str() + eq + 1);
+        else if (!kv.empty()) fprintf(stderr, "liblamb: LAMB_TUNE: unknown entry '%s' ignored\n", kv.c_str());
+        pos = end + 1;
     }
     return t;
-}();
-
-template <int NS, int U, int M>
-static cudaError_t pass_a_v(const StepParams& p, int grid, cudaStream_t s) {
-    pass_a_kernel<NS, U, M><<<grid, kThreads, 0, s>>>(p);
-    return cudaGetLastError();
 }
-template <int NS, int U>
-static cudaError_t pass_a_pf(const StepParams& p, int grid, cudaStream_t s) {
-    pass_a_pf_kernel<NS, U, 2><<<grid, kThreads, 0, s>>>(p);
-    return cudaGetLastError();
-}
+static const Tune g_tune = parse_tune();
 
 // Dynamic shared memory above 48 KB must be opted into per kernel AND per device (the attribute
 // lives in the device's context): a process may drive handles on several GPUs, so the opt-in is
@@ -1243,188 +999,99 @@ static void set_smem_once(std::atomic<uint64_t>& done, const void* kernel, size_
     done.fetch_or(bit, std::memory_order_acq_rel);
 }
 
-template <int NS, int U, int PD>
-static cudaError_t pass_a_ring(const StepParams& p, int grid, cudaStream_t s) {
-    const size_t smem = (size_t)(kThreads / 32) * PD * U * NS * 32 * sizeof(uint2);
-    static std::atomic<uint64_t> attr{0};
-    set_smem_once(attr, (const void*)pass_a_ring_kernel<NS, U, PD>, smem);
-    pass_a_ring_kernel<NS, U, PD><<<grid, kThreads, smem, s>>>(p);
-    return cudaGetLastError();
-}
-
-// one CTA per SM (the ring uses ~170 KB of shared memory); `grid` (the SM budget) caps it
-static int tma_grid(int grid) {
+// Persistent grids.  TMA kernels: one CTA per SM (their ring takes most of the shared memory);
+// the LDG kernels: SMs x resident CTAs from the occupancy calculator.  `budget` (> 0) caps the
+// CTA count (lamb_set_max_ctas: leave SMs to concurrent compute).
+static int sm_count() {
     int dev = 0, sms = 0;   // the current device's SM count (cached by the runtime)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return grid < sms ? grid : sms;
+    return sms;
+}
+static int capped(int grid, int budget) { return budget > 0 && budget < grid ? budget : grid; }
+template <typename K>
+static int occupancy_grid(K kernel) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+    return sm_count() * (per_sm < 1 ? 1 : per_sm);
 }
 
 template <int NS>
-static cudaError_t pass_a_tma(const StepParams& p, int grid, cudaStream_t s) {
+static cudaError_t pass_a_tma(const StepParams& p, int budget, cudaStream_t s) {
     const size_t smem = sizeof(TmaStage<NS>) * tma_stages_a<NS>() + 2 * tma_stages_a<NS>() * sizeof(uint64_t);
     static std::atomic<uint64_t> attr{0};
     set_smem_once(attr, (const void*)pass_a_tma_kernel<NS>, smem);
-    pass_a_tma_kernel<NS><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
-    return cudaGetLastError();
-}
-
-template <int NS, int SS, bool OWN>
-static cudaError_t pass_a_tma2(const StepParams& p, int grid, cudaStream_t s) {
-    constexpr int NR = OWN ? NS - 1 : NS;
-    constexpr int GS = tma2_grad_stages<NS, SS, OWN>();
-    const size_t smem = sizeof(TmaStateStage<OWN>) * SS + sizeof(TmaGradStage<NR>) * GS + 2 * (SS + GS) * sizeof(uint64_t);
-    static std::atomic<uint64_t> attr{0};
-    set_smem_once(attr, (const void*)pass_a_tma2_kernel<NS, SS, OWN>, smem);
-    pass_a_tma2_kernel<NS, SS, OWN><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
+    pass_a_tma_kernel<NS><<<capped(sm_count(), budget), kTmaConsumers + 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 template <int NS>
-static cudaError_t pass_a_ns(const StepParams& p, int grid, cudaStream_t s) {
-    const Tune& t = g_tune;
-    if constexpr (NS >= 2) {
-        if (p.staged) {   // copy-engine schedule: only the TMA kernels address staging by shard offset
-            if constexpr (NS == 2) return pass_a_tma2<NS, 2, true>(p, grid, s);
-            else return pass_a_tma<NS>(p, grid, s);
-        }
-    }
-    if constexpr (NS == 2) {
-        if (t.tma_multi == 1) return pass_a_tma2<NS, 2, true>(p, grid, s);   // the D = 2 default
-        // (tmam=6: the single ring at D = 2, for A/B runs)
-    }
-    if constexpr (NS >= 2 && NS <= 4) {
-        // tmam=2: state ring 3 deep at D = 2 (2 beyond); tmam=3: state ring 2 deep, grads
-        // further ahead (6 items at D = 2); tmam=4/5: own slice in the state ring (2 / 3 deep),
-        // only remote slices in the deep ring
-        if (t.tma_multi == 2) return pass_a_tma2<NS, NS <= 2 ? 3 : 2, false>(p, grid, s);
-        if (t.tma_multi == 3) return pass_a_tma2<NS, 2, false>(p, grid, s);
-        if (t.tma_multi == 4) return pass_a_tma2<NS, 2, true>(p, grid, s);
-        if constexpr (NS == 2) {
-            if (t.tma_multi == 5) return pass_a_tma2<NS, 3, true>(p, grid, s);
-        }
-    }
-    if constexpr (NS >= 1) {
-        if (NS == 1 ? t.tma : t.tma_multi) return pass_a_tma<NS>(p, grid, s);
-    }
-    if constexpr (NS == 2) {
-        if (t.tma_multi == 1) return pass_a_tma2<NS, 2, true>(p, grid, s);   // the D = 2 default
-        // (tmam=6: the single ring at D = 2, for A/B runs)
-    }
-    if constexpr (NS >= 2 && NS <= 4) {
-        if (t.ring == 3) return pass_a_ring<NS, 4, 3>(p, grid, s);
-        if (t.ring == 4) return pass_a_ring<NS, 4, 4>(p, grid, s);
-        if (t.ring == 6) return pass_a_ring<NS, 2, 6>(p, grid, s);
-    }
-    if constexpr (NS >= 2) {
-        if (t.pf) {
-            if constexpr (NS == 2) {   // U = 4 fits the register budget only for two sources
-                if (t.upf == 4) return pass_a_pf<NS, 4>(p, grid, s);
-            }
-            return pass_a_pf<NS, 2>(p, grid, s);
-        }
-    }
-    if (t.ua == 2 && t.ma == 4) return pass_a_v<NS, 2, 4>(p, grid, s);
-    if (t.ua == 2 && t.ma == 3) return pass_a_v<NS, 2, 3>(p, grid, s);
-    if (t.ua == 4 && t.ma == 3) return pass_a_v<NS, 4, 3>(p, grid, s);
-    if (t.ua == 4 && t.ma == 4) return pass_a_v<NS, 4, 4>(p, grid, s);
-    return pass_a_v<NS, 4, 2>(p, grid, s);
+static cudaError_t pass_a_tma2(const StepParams& p, int budget, cudaStream_t s) {
+    constexpr int SS = 2;
+    constexpr int GS = tma2_grad_stages<NS, SS, true>();
+    const size_t smem = sizeof(TmaStateStage<true>) * SS + sizeof(TmaGradStage<NS - 1>) * GS + 2 * (SS + GS) * sizeof(uint64_t);
+    static std::atomic<uint64_t> attr{0};
+    set_smem_once(attr, (const void*)pass_a_tma2_kernel<NS, SS, true>, smem);
+    pass_a_tma2_kernel<NS, SS, true><<<capped(sm_count(), budget), kTmaConsumers + 32, smem, s>>>(p);
+    return cudaGetLastError();
 }
 
-cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int grid, cudaStream_t s) {
+template <int NS>
+static cudaError_t pass_a_ns(const StepParams& p, int budget, cudaStream_t s) {
+    if constexpr (NS == 0) {
+        pass_a_kernel<0, 4, 2><<<capped(occupancy_grid(pass_a_kernel<0, 4, 2>), budget), kThreads, 0, s>>>(p);
+        return cudaGetLastError();
+    } else if constexpr (NS >= 2 && NS <= 4) {
+        const bool decoupled = g_tune.tmam < 0 ? NS == 2 : g_tune.tmam == 1;
+        return decoupled ? pass_a_tma2<NS>(p, budget, s) : pass_a_tma<NS>(p, budget, s);
+    } else {
+        return pass_a_tma<NS>(p, budget, s);
+    }
+}
+
+cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int budget, cudaStream_t s) {
     if (p.item_end <= p.item_begin) return cudaSuccess;
-    if (g32) return pass_a_ns<0>(p, grid, s);
+    if (g32) return pass_a_ns<0>(p, budget, s);
     switch (nsrc) {
-        case 1: return pass_a_ns<1>(p, grid, s);
-        case 2: return pass_a_ns<2>(p, grid, s);
-        case 3: return pass_a_ns<3>(p, grid, s);
-        case 4: return pass_a_ns<4>(p, grid, s);
-        case 5: return pass_a_ns<5>(p, grid, s);
-        case 6: return pass_a_ns<6>(p, grid, s);
-        case 7: return pass_a_ns<7>(p, grid, s);
-        case 8: return pass_a_ns<8>(p, grid, s);
+        case 1: return pass_a_ns<1>(p, budget, s);
+        case 2: return pass_a_ns<2>(p, budget, s);
+        case 3: return pass_a_ns<3>(p, budget, s);
+        case 4: return pass_a_ns<4>(p, budget, s);
+        case 5: return pass_a_ns<5>(p, budget, s);
+        case 6: return pass_a_ns<6>(p, budget, s);
+        case 7: return pass_a_ns<7>(p, budget, s);
+        case 8: return pass_a_ns<8>(p, budget, s);
     }
     return cudaErrorInvalidValue;
-}
-
-template <int ND, int U, int M>
-static cudaError_t pass_b_v(const StepParams& p, int grid, cudaStream_t s) {
-    pass_b_kernel<ND, U, M><<<grid, kThreads, 0, s>>>(p);
-    return cudaGetLastError();
-}
-template <int ND, bool BULK>
-static cudaError_t pass_b_tma(const StepParams& p, int grid, cudaStream_t s) {
-    const size_t smem = sizeof(TmaStageB) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t) + 64 +
-                        (BULK ? sizeof(TmaParamStage) * kTmaStages : 0);
-    static std::atomic<uint64_t> attr{0};
-    set_smem_once(attr, (const void*)pass_b_tma_kernel<ND, BULK>, smem);
-    pass_b_tma_kernel<ND, BULK><<<tma_grid(grid), kTmaConsumers + 32, smem, s>>>(p);
-    return cudaGetLastError();
 }
 
 template <int ND>
-static cudaError_t pass_b_nd(const StepParams& p, int grid, cudaStream_t s) {
-    const Tune& t = g_tune;
-    if (t.tmb) return pass_b_tma<ND, true>(p, grid, s);   // bulk param stores (LAMB_TUNE tmb=1)
-    if (ND == 1 ? t.tma : t.tma_multi) return pass_b_tma<ND, false>(p, grid, s);
-    if (t.ub == 2 && t.mb == 4) return pass_b_v<ND, 2, 4>(p, grid, s);
-    if (t.ub == 2 && t.mb == 3) return pass_b_v<ND, 2, 3>(p, grid, s);
-    if (t.ub == 4 && t.mb == 3) return pass_b_v<ND, 4, 3>(p, grid, s);
-    if (t.ub == 4 && t.mb == 4) return pass_b_v<ND, 4, 4>(p, grid, s);
-    return pass_b_v<ND, 4, 2>(p, grid, s);
+static cudaError_t pass_b_tma(const StepParams& p, int budget, cudaStream_t s) {
+    const size_t smem = sizeof(TmaStageB) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
+    static std::atomic<uint64_t> attr{0};
+    set_smem_once(attr, (const void*)pass_b_tma_kernel<ND>, smem);
+    pass_b_tma_kernel<ND><<<capped(sm_count(), budget), kTmaConsumers + 32, smem, s>>>(p);
+    return cudaGetLastError();
 }
 
-cudaError_t launch_pass_b(const StepParams& p, int ndst, int grid, cudaStream_t s) {
+cudaError_t launch_pass_b(const StepParams& p, int ndst, int budget, cudaStream_t s) {
     if (p.item_end <= p.item_begin) return cudaSuccess;
     switch (ndst) {
-        case 1: return pass_b_nd<1>(p, grid, s);
-        case 2: return pass_b_nd<2>(p, grid, s);
-        case 3: return pass_b_nd<3>(p, grid, s);
-        case 4: return pass_b_nd<4>(p, grid, s);
-        case 5: return pass_b_nd<5>(p, grid, s);
-        case 6: return pass_b_nd<6>(p, grid, s);
-        case 7: return pass_b_nd<7>(p, grid, s);
-        case 8: return pass_b_nd<8>(p, grid, s);
+        case 1: return pass_b_tma<1>(p, budget, s);
+        case 2: return pass_b_tma<2>(p, budget, s);
+        case 3: return pass_b_tma<3>(p, budget, s);
+        case 4: return pass_b_tma<4>(p, budget, s);
+        case 5: return pass_b_tma<5>(p, budget, s);
+        case 6: return pass_b_tma<6>(p, budget, s);
+        case 7: return pass_b_tma<7>(p, budget, s);
+        case 8: return pass_b_tma<8>(p, budget, s);
     }
     return cudaErrorInvalidValue;
 }
 
-template <typename K>
-static int occupancy_grid(int device, K kernel) {
-    int sms = 0, per_sm = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
-    if (per_sm < 1) per_sm = 1;
-    return sms * per_sm;
-}
-
-int pass_grid(int device, int nsrc, bool g32, bool pass_b, int ndst) {
-    // persistent grid: SMs x resident CTAs of the variant that will run
-    (void)g32;
-    const Tune& t = g_tune;
-    auto pick_a = [&](auto ns) -> int {
-        constexpr int NS = decltype(ns)::value;
-        if (t.ua == 2 && t.ma == 4) return occupancy_grid(device, pass_a_kernel<NS, 2, 4>);
-        if (t.ua == 2 && t.ma == 3) return occupancy_grid(device, pass_a_kernel<NS, 2, 3>);
-        if (t.ua == 4 && t.ma == 3) return occupancy_grid(device, pass_a_kernel<NS, 4, 3>);
-        if (t.ua == 4 && t.ma == 4) return occupancy_grid(device, pass_a_kernel<NS, 4, 4>);
-        return occupancy_grid(device, pass_a_kernel<NS, 4, 2>);
-    };
-    auto pick_b = [&](auto nd) -> int {
-        constexpr int ND = decltype(nd)::value;
-        if (t.ub == 2 && t.mb == 4) return occupancy_grid(device, pass_b_kernel<ND, 2, 4>);
-        if (t.ub == 2 && t.mb == 3) return occupancy_grid(device, pass_b_kernel<ND, 2, 3>);
-        if (t.ub == 4 && t.mb == 3) return occupancy_grid(device, pass_b_kernel<ND, 4, 3>);
-        if (t.ub == 4 && t.mb == 4) return occupancy_grid(device, pass_b_kernel<ND, 4, 4>);
-        return occupancy_grid(device, pass_b_kernel<ND, 4, 2>);
-    };
-    if (pass_b) return ndst <= 1 ? pick_b(std::integral_constant<int, 1>()) : pick_b(std::integral_constant<int, 8>());
-    return nsrc <= 1 ? pick_a(std::integral_constant<int, 1>()) : pick_a(std::integral_constant<int, 8>());
-}
-
 template <int NS, bool MAT>
-static cudaError_t grad_stats_v(const StepParams& p, int grid, cudaStream_t s) {
-    grad_stats_kernel<NS, MAT><<<grid, kThreads, 0, s>>>(p);
+static cudaError_t grad_stats_v(const StepParams& p, int budget, cudaStream_t s) {
+    grad_stats_kernel<NS, MAT><<<capped(occupancy_grid(grad_stats_kernel<NS, MAT>), budget), kThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 

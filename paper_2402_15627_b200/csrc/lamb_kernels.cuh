@@ -124,16 +124,18 @@ struct GroupTable {
     GroupConst g[LAMB_MAX_GROUPS];
 };
 
-// Host launchers (lamb_kernels.cu).  `occ_grid` = persistent grid size.
+// Host launchers (lamb_kernels.cu).  The streaming passes size their own persistent grids
+// (TMA kernels: one CTA per SM; LDG kernels: SMs x resident CTAs); `budget` > 0 caps the CTA
+// count (lamb_set_max_ctas), 0 = a full wave.
 cudaError_t launch_self_check(const Item* items, int64_t n_items, const float* w, const float* m, const float* v,
                               const __nv_bfloat16* grad, const __nv_bfloat16* param, const int64_t* shard_pad,
                               int64_t n_shard_pad, const int64_t* flat_pad, int64_t n_flat_pad,
                               const uint64_t* const* peer_flags, int world, unsigned long long* out,
                               cudaStream_t s);
 cudaError_t launch_prologue(const GroupTable& t, int n_groups, GroupConst* dst, cudaStream_t s);
-cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int grid, cudaStream_t s);
-cudaError_t launch_pass_b(const StepParams& p, int ndst, int grid, cudaStream_t s);
-cudaError_t launch_grad_stats(const StepParams& p, int nsrc, bool materialise, int grid, cudaStream_t s);
+cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int budget, cudaStream_t s);
+cudaError_t launch_pass_b(const StepParams& p, int ndst, int budget, cudaStream_t s);
+cudaError_t launch_grad_stats(const StepParams& p, int nsrc, bool materialise, int budget, cudaStream_t s);
 cudaError_t launch_clip_finalize(const ClipParams& p, cudaStream_t s);
 cudaError_t launch_clip_combine(const ClipParams& p, cudaStream_t s);
 cudaError_t launch_finalize_segments(const FinalizeParams& p, cudaStream_t s);
@@ -149,6 +151,5 @@ cudaError_t launch_flag_wait(const uint64_t* flags, int64_t b0, int64_t b1, int 
                              int* err_flag, uint64_t timeout_ns, cudaStream_t s);
 cudaError_t launch_upcast_bf16(const __nv_bfloat16* src, float* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_cast_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t s);
-int pass_grid(int device, int nsrc, bool g32, bool pass_b, int ndst);
 
 }  // namespace lamb

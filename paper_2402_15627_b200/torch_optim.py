@@ -22,10 +22,14 @@ staging as soon as the backward has produced all of them (`lamb_push_grads_bucke
 runs `lamb_step_staged` (the all-gather then streams into the next forward), and a global
 module forward-pre-hook makes the forward of a module wait for the buckets its own parameters
 live in (`lamb_wait_params_bucket`).  Parameters must therefore be used through `nn.Module`
-forwards; results are bit-identical to `overlap=False`.
+forwards; results are bit-identical to `overlap=False`.  Gradient accumulation: run every
+micro-batch but the last under `with opt.no_sync():` (as with DDP) — the buckets are pushed by
+the last backward only, once their gradients are final.  A second backward outside `no_sync()`
+before `step()` raises instead of reducing a partial gradient.
 """
 from __future__ import annotations
 
+import contextlib
 from typing import Iterable, List, Optional
 
 import torch
@@ -38,7 +42,7 @@ class LambOptimizer:
                  weight_decay: float = 0.0, adapt: bool = True, bias_correction: bool = True,
                  world_size: int = 1, rank: int = 0, pg=None, comm_mode: int = lamb.LAMB_COMM_FUSED,
                  bucket_cap: int = 0, max_grad_norm: float = 0.0, graph: bool = False,
-                 overlap: bool = False):
+                 overlap: bool = False, bootstrap: str = "nccl"):
         params = list(params)
         if params and not isinstance(params[0], dict):
             params = [{"params": params}]
@@ -67,7 +71,8 @@ class LambOptimizer:
         if self.overlap and (comm_mode != lamb.LAMB_COMM_FUSED or max_grad_norm > 0):
             raise ValueError("overlap=True needs comm_mode=FUSED and no global clipping")
         self.L = lamb.Lamb(table, self.groups, world_size=world_size, rank=rank, device=self.device,
-                           comm_mode=comm_mode, bucket_cap=bucket_cap, pg=pg, graph=graph, ce=self.overlap)
+                           comm_mode=comm_mode, bucket_cap=bucket_cap, pg=pg, graph=graph, ce=self.overlap,
+                           bootstrap=bootstrap)
         # fp32 master = the current bf16 values (exact), then the params become buffer views
         flat = torch.zeros(self.L.plan.flat_size, dtype=torch.float32, device=f"cuda:{self.device}")
         for p, off in zip(self.params, self.L.plan.tensor_off.tolist()):
@@ -92,6 +97,21 @@ class LambOptimizer:
                                  push=self.L.push_grads_bucket, wait=self.L.wait_params_bucket,
                                  grad_views=[g.view(p.shape) for p, g in zip(self.params, self.L.grad_views())])
         self._hooks = self._ov.install()
+
+    @contextlib.contextmanager
+    def no_sync(self):
+        """Backward passes inside this context only accumulate into the grad buffer (gradient
+        accumulation micro-batches); with overlap=True they push nothing to the peers.  The
+        backward of the last micro-batch runs outside it.  With overlap=False a no-op."""
+        if not self.overlap:
+            yield
+            return
+        prev = self._ov.sync
+        self._ov.sync = False
+        try:
+            yield
+        finally:
+            self._ov.sync = prev
 
     def wait_params(self) -> None:
         """Make the current stream wait for every bucket's all-gather (e.g. before using the
@@ -135,6 +155,8 @@ class LambOptimizer:
 
     def load_path(self, path: str) -> None:
         self.t = self.L.checkpoint_load(path)
+        if self.overlap:   # the load rebuilt every param buffer: nothing to wait for or push
+            self._ov.reset(self.t)
 
 
 class BucketOverlap:
@@ -144,7 +166,10 @@ class BucketOverlap:
     per forward after a staged step: `wait(b, t_staged)` once per bucket, right before the first
     module whose own parameters live in bucket b runs (a global module forward-pre-hook).
     `before_step` pushes buckets whose parameters got no gradient and waits for buckets no
-    module used; `after_step` arms the next forward's waits."""
+    module used; `after_step` arms the next forward's waits.  While `sync` is False (the
+    optimizer's no_sync(): accumulation micro-batches) the hooks push nothing; a bucket whose
+    parameters receive gradients again after it was pushed raises (its pushed copy would be
+    partial, and the copy engine may still be reading the buffer the backward writes)."""
 
     def __init__(self, params, bucket_of, n_buckets: int, push, wait, grad_views=None):
         self.params = list(params)
@@ -161,6 +186,7 @@ class BucketOverlap:
         self.staged = 0
         self.awaited = [True] * n_buckets
         self.t_next = 1
+        self.sync = True
 
     def install(self):
         hooks = []
@@ -177,6 +203,13 @@ class BucketOverlap:
             if gview is not None and param.grad is not None and param.grad.data_ptr() != gview.data_ptr():
                 gview.copy_(param.grad)   # autograd replaced .grad: back into the library buffer
                 param.grad = gview
+            if not self.sync:
+                return
+            if self.pushed[b]:
+                raise RuntimeError(
+                    f"bucket {b} received gradients after it was pushed to the peers in this step: "
+                    "with LambOptimizer(overlap=True) run the backward of every micro-batch but the "
+                    "last under `with opt.no_sync():`")
             self.pending[b] -= 1
             if self.pending[b] == 0 and not self.pushed[b]:
                 self.push(b, self.t_next)
@@ -205,6 +238,14 @@ class BucketOverlap:
             if not self.pushed[b]:
                 self.push(b, t)
                 self.pushed[b] = True
+
+    def reset(self, t: int):
+        """After a checkpoint load at step t: no pending waits, the next pushes are step t+1."""
+        self.staged = 0
+        self.t_next = t + 1
+        self.pending = list(self.size)
+        self.pushed = [False] * self.n
+        self.awaited = [True] * self.n
 
     def after_step(self, t: int):
         self.staged = t

@@ -21,7 +21,7 @@ import torch.distributed as dist  # noqa: E402
 
 import oracle  # noqa: E402
 import workloads as W  # noqa: E402
-from gpu_common import compare_state, spec_of  # noqa: E402
+from gpu_common import compare_state, snapshot_w, spec_of  # noqa: E402
 
 
 # "nccl": one rank per GPU, NCCL bootstrap.  "host" (--oversub): D ranks over fewer GPUs
@@ -58,6 +58,8 @@ def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, chec
     L.synth_init(spec, wl.seed)
     for t in range(1, steps + 1):
         L.synth_grads(spec, wl.seed, rank + 1, t)
+        if t == steps:
+            L.w_prev = snapshot_w(L, ids)   # per-step update check of the last step
         L.step(t)
     torch.cuda.synchronize()
     orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK, tensor_ids=ids)
@@ -100,11 +102,12 @@ def clip_case(world, rank, local, mode):
     gn1 = np.sqrt(sum(np.sum(orc.grads(i, 1) ** 2) for i in orc.ids))
     max_norm = float(np.float32(0.3 * gn1))
     L = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
-                  device=local, comm_mode=mode, bucket_cap=8192, pg=dist.group.WORLD)
+                  device=local, comm_mode=mode, bucket_cap=8192, pg=dist.group.WORLD, bootstrap=BOOT)
     L.synth_init(spec, wl.seed)
     L.set_grad_clip(max_norm)
     for t in (1, 2):
         L.synth_grads(spec, wl.seed, rank + 1, t)
+        L.w_prev = snapshot_w(L)
         L.step(t)
         info = orc.step(t, max_grad_norm=max_norm)
         gi = L.step_info()
@@ -133,15 +136,18 @@ def bucket_case(world, rank, local, mode):
     wl = W.Workload("bkd", 73, tensors, W.default_groups(lr=2.0 ** -7))
     spec = spec_of(wl)
     mk = lambda: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
-                           device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD)
+                           device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD, bootstrap=BOOT)
     A, B = mk(), mk()
     nb = len(A.plan.buckets)
+    assert nb > 3
     for L in (A, B):
         L.synth_init(spec, wl.seed)
     for t in (1, 2):
         for L in (A, B):
             L.synth_grads(spec, wl.seed, rank + 1, t)
         A.step(t)
+        if t == 2:
+            B.w_prev = snapshot_w(B)
         for b in reversed(range(nb)):
             B.step_bucket(b, t, defer_ag=True)
         for b in range(nb):
@@ -150,11 +156,17 @@ def bucket_case(world, rank, local, mode):
     for k in (2, 3, 4):
         assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32)), k
     assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
+    # and against the oracle (per-bucket stepping is the exact LAMB step)
+    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+    for t in (1, 2):
+        orc.step(t)
+    compare_state(B, orc, 2, check_params=False)
     A.close()
     B.close()
     dist.barrier()
     if rank == 0:
-        print(f"[ok] per-bucket stepping D={world} mode={mode} buckets={nb} == lamb_step (bitwise)", flush=True)
+        print(f"[ok] per-bucket stepping D={world} mode={mode} buckets={nb} == lamb_step (bitwise) == oracle",
+              flush=True)
 
 
 def host_case(world, rank, local, mode):
@@ -166,7 +178,7 @@ def host_case(world, rank, local, mode):
     wl = W.Workload("hostd", 74, tensors, W.default_groups(lr=2.0 ** -7))
     spec = spec_of(wl)
     mk = lambda: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
-                           device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD)
+                           device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD, bootstrap=BOOT)
     A, B = mk(), mk()
     for L in (A, B):
         L.synth_init(spec, wl.seed)
@@ -221,6 +233,7 @@ def ckpt_case(world, rank, local, mode):
     B = mk(world, rank, 5000, dist.group.WORLD)
     assert B.checkpoint_load(path) == 2
     B.synth_grads(spec, wl.seed, rank + 1, 3)
+    B.w_prev = snapshot_w(B)
     B.step(3)
     torch.cuda.synchronize()
     compare_state(B, orc, 3, check_params=False)
@@ -252,7 +265,8 @@ def graph_case(world, rank, local, mode):
     wl = W.Workload("graphd", 75, tensors, W.default_groups(lr=2.0 ** -7))
     spec = spec_of(wl)
     mk = lambda g: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
-                             device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD, graph=g)
+                             device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD, graph=g,
+                             bootstrap=BOOT)
     E, G = mk(False), mk(True)
     for L in (E, G):
         L.synth_init(spec, wl.seed)
@@ -315,11 +329,73 @@ def ce_case(world, rank, local, mode):
         assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32)), k
     assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
     assert all(v == 0 for v in A.self_check().values()), A.self_check()
+    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+    for t in (1, 2, 3, 4):
+        orc.step(t)
+    compare_state(A, orc, 4, check_params=False)
     A.close()
     B.close()
     dist.barrier()
     if rank == 0:
-        print(f"[ok] copy-engine schedule D={world} ({nb} buckets, 4 steps) == lamb_step (bitwise)", flush=True)
+        print(f"[ok] copy-engine schedule D={world} ({nb} buckets, 4 steps) == lamb_step (bitwise) == oracle",
+              flush=True)
+
+
+def ce_rollback_case(world, rank, local, mode):
+    """Copy-engine schedule across a rollback: checkpoint after step 2, run step 3,
+    reload step 2 and run steps 3 and 4 again — the arrival flags carry an internal round
+    number, so the repeated step numbers cannot release a wait early.  Bitwise equal to an
+    uninterrupted lamb_step run."""
+    from paper_2402_15627_b200 import lamb
+    if mode != lamb.LAMB_COMM_FUSED:
+        return
+    rng = np.random.default_rng(507)
+    tensors = W.random_table(rng, 40, max_numel=7000, p_big=0.2, big=50_000)
+    wl = W.Workload("cerb", 80, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    mk = lambda ce: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
+                              device=local, comm_mode=mode, bucket_cap=12_000, pg=dist.group.WORLD,
+                              bootstrap=BOOT, ce=ce)
+    A, B = mk(True), mk(False)
+    A.synth_init(spec, wl.seed)
+    B.synth_init(spec, wl.seed)
+    nb = A.plan.buckets.shape[0]
+    path = f"/tmp/lamb_cerb_D{world}.bin"
+
+    def ce_step(t, wait_for):
+        if wait_for:
+            for b in range(nb):
+                A.wait_params_bucket(b, wait_for)
+        A.synth_grads(spec, wl.seed, rank + 1, t)
+        for b in reversed(range(nb)):
+            A.push_grads_bucket(b, t)
+        A.step_staged(t)
+
+    ce_step(1, 0)
+    ce_step(2, 1)
+    A.checkpoint_save(path, 2)
+    A.checkpoint_wait()
+    dist.barrier()
+    ce_step(3, 2)
+    for b in range(nb):
+        A.wait_params_bucket(b, 3)
+    assert A.checkpoint_load(path) == 2       # rollback: params rebuilt, nothing to wait for
+    ce_step(3, 0)
+    ce_step(4, 3)
+    for b in range(nb):
+        A.wait_params_bucket(b, 4)
+    for t in (1, 2, 3, 4):
+        B.synth_grads(spec, wl.seed, rank + 1, t)
+        B.step(t)
+    torch.cuda.synchronize()
+    for k in (2, 3, 4):
+        assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32)), k
+    assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
+    A.close()
+    B.close()
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] copy-engine schedule across a checkpoint rollback D={world} == lamb_step (bitwise)", flush=True)
 
 
 def replicated_case(world, rank, local, mode):
@@ -337,6 +413,8 @@ def replicated_case(world, rank, local, mode):
     steps = 10
     for t in range(1, steps + 1):
         L.synth_grads(spec, wl.seed, oracle.rank_term(oracle.REPLICATED, rank), t)
+        if t == steps:
+            L.w_prev = snapshot_w(L)
         L.step(t)
     torch.cuda.synchronize()
     orc = oracle.OracleRun(wl, world_size=1, mode=oracle.REPLICATED)
@@ -392,7 +470,7 @@ def h10_case(world, rank, local, mode):
     wl = W.Workload("h10", 76, tensors, W.default_groups(lr=2.0 ** -7))
     spec = spec_of(wl)
     L = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank, device=local,
-                  comm_mode=mode, bucket_cap=10_000, pg=dist.group.WORLD)
+                  comm_mode=mode, bucket_cap=10_000, pg=dist.group.WORLD, bootstrap=BOOT)
     L.synth_init(spec, wl.seed)
     if mode == lamb.LAMB_COMM_FUSED:
         L.set_grad_clip(1e30)            # the fused path materialises the sum in its pre-step
@@ -421,14 +499,14 @@ def torch_case(world, rank, local, mode):
     ordered = [p for _, p in model.named_parameters()]
     w0 = [p.detach().double().cpu().numpy().reshape(-1).copy() for p in ordered]
     opt = LambOptimizer(model.parameters(), lr=2.0 ** -7, weight_decay=0.01, world_size=world, rank=rank,
-                        pg=dist.group.WORLD, comm_mode=mode, bucket_cap=5000)
+                        pg=dist.group.WORLD, comm_mode=mode, bucket_cap=5000, bootstrap=BOOT)
     g_all = []
     torch.manual_seed(1 + rank)          # different data per rank
     for _ in range(2):
         x = torch.randn(32, 64, device="cuda", dtype=torch.bfloat16)
         opt.zero_grad()
         model(x).float().pow(2).mean().backward()
-        mine = torch.cat([p.grad.detach().reshape(-1).float() for p in ordered])
+        mine = torch.cat([p.grad.detach().reshape(-1).float() for p in ordered]).to(_dev())
         gathered = [torch.empty_like(mine) for _ in range(world)]
         dist.all_gather(gathered, mine)
         g_all.append(torch.stack(gathered).double().cpu().numpy())
@@ -453,7 +531,7 @@ def torch_case(world, rank, local, mode):
             r = ref[toff:toff + ln]
             assert np.all(np.abs(gg - r) <= atol + 1e-4 * np.abs(r)), i
     # every rank's model now holds the same (all-gathered) parameters
-    flat = torch.cat([p.detach().reshape(-1) for p in ordered]).view(torch.int16).long()
+    flat = torch.cat([p.detach().reshape(-1) for p in ordered]).view(torch.int16).long().to(_dev())
     hs = [torch.empty_like(flat) for _ in range(world)]
     dist.all_gather(hs, flat)
     assert all(torch.equal(h, hs[0]) for h in hs)
@@ -478,7 +556,7 @@ def torch_overlap_case(world, rank, local, mode):
                                    torch.nn.GELU(), torch.nn.Linear(200, 17)).cuda().bfloat16()
     mA, mB = build(), build()
     kw = dict(lr=2.0 ** -7, weight_decay=0.01, world_size=world, rank=rank, pg=dist.group.WORLD,
-              comm_mode=mode, bucket_cap=9000)
+              comm_mode=mode, bucket_cap=9000, bootstrap=BOOT)
     oA, oB = LambOptimizer(mA.parameters(), overlap=True, **kw), LambOptimizer(mB.parameters(), **kw)
     assert oA.L.plan.buckets.shape[0] > 2
     torch.manual_seed(1 + rank)
@@ -568,9 +646,17 @@ def main():
         run_case("stress", W.Workload("stress", 51, stress, W.default_groups()), world, rank, local, mode, 2,
                  cap=100_000)
         ckpt_case(world, rank, local, mode)
+        clip_case(world, rank, local, mode)
+        bucket_case(world, rank, local, mode)
+        host_case(world, rank, local, mode)
+        graph_case(world, rank, local, mode)
+        h10_case(world, rank, local, mode)
         hide_case(world, rank, local, mode)
         replicated_case(world, rank, local, mode)
         ce_case(world, rank, local, mode)
+        ce_rollback_case(world, rank, local, mode)
+        torch_case(world, rank, local, mode)
+        torch_overlap_case(world, rank, local, mode)
         dist.barrier()
         dist.destroy_process_group()
         return
@@ -616,6 +702,7 @@ def main():
     hide_case(world, rank, local, mode)
     replicated_case(world, rank, local, mode)
     ce_case(world, rank, local, mode)
+    ce_rollback_case(world, rank, local, mode)
     torch_case(world, rank, local, mode)
     torch_overlap_case(world, rank, local, mode)
     os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"

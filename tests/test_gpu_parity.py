@@ -8,7 +8,7 @@ import pytest
 
 import oracle
 import workloads as W
-from gpu_common import compare_state, run_gpu, spec_of
+from gpu_common import compare_state, run_gpu, snapshot_w, spec_of
 
 torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu,
@@ -46,14 +46,20 @@ def test_generator_matches_oracle_bit_exact(lamb):
     L.close()
 
 
+@pytest.mark.parametrize("lr", [2.0 ** -10, 2.0 ** -7])
 @pytest.mark.parametrize("steps", [1, 10])
-def test_toy_parity(lamb, steps):
+def test_toy_parity(lamb, steps, lr):
+    """BASELINE configs[0] at the bench lr and at the hand-case lr: w, m, v, params, ratios and
+    the last step's per-element update against the oracle."""
     wl = W.toy()
+    wl.groups = W.default_groups(lr=lr)
     L = run_gpu(wl, steps=steps)
     orc = oracle.OracleRun(wl, world_size=1, mode=oracle.PER_RANK)
     for t in range(1, steps + 1):
         orc.step(t)
     compare_state(L, orc, steps)
+    print(f"toy steps={steps} lr={lr}: update check max |err|/allowed = {L.update_worst:.3f}")
+    assert 0.0 < L.update_worst <= 1.0
     L.close()
 
 
@@ -175,6 +181,7 @@ def test_set_master_and_step_host(lamb):
         o = int(L.plan.tensor_off[i])
         flat[o:o + ts.numel] = torch.from_numpy(orc.w[i]).float()
     L.set_master(flat)
+    L.w_prev = snapshot_w(L)
     L.synth_grads(spec_of(wl), wl.seed, 1, 1)
     hg = L.grad_buffer().cpu().pin_memory()
     hp = torch.empty(L.plan.flat_size, dtype=torch.bfloat16).pin_memory()
@@ -198,10 +205,11 @@ def test_gpt13b_layout_1p3b_full_size_sampled(lamb):
     L.synth_init(spec, wl.seed)
     L.synth_grads(spec, wl.seed, 1, 1)
     w_before = L.state_buffer(Lm.LAMB_BUF_W).clone()
+    ids = [0] + list(range(1, 13)) + [len(wl.tensors) - 2, len(wl.tensors) - 1]
+    L.w_prev = snapshot_w(L, ids)
     L.step(1)
     torch.cuda.synchronize()
     w_after = L.state_buffer(Lm.LAMB_BUF_W)
-    ids = [0] + list(range(1, 13)) + [len(wl.tensors) - 2, len(wl.tensors) - 1]
     orc = oracle.OracleRun(wl, world_size=1, tensor_ids=ids)
     orc.step(1)
     compare_state(L, orc, 1, ids=ids)
@@ -342,6 +350,7 @@ def test_prestep_clip_and_loss_scale(lamb, frac, inv_scale):
     L.set_loss_scale(inv_scale)
     for t in (1, 2, 3):
         L.synth_grads(spec, wl.seed, 1, t)
+        L.w_prev = snapshot_w(L)
         if S != 1.0:
             g = L.grad_buffer()
             g.copy_((g.float() * S).bfloat16())
@@ -397,6 +406,8 @@ def test_step_bucket_equals_step(lamb, defer):
         for L in (A, B):
             L.synth_grads(spec, wl.seed, 1, t)
         A.step(t)
+        if t == 3:
+            B.w_prev = snapshot_w(B)
         for b in reversed(range(nb)):
             B.step_bucket(b, t, defer_ag=defer)
         if defer:
@@ -406,6 +417,10 @@ def test_step_bucket_equals_step(lamb, defer):
     for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V):
         assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32))
     assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
+    orc = oracle.OracleRun(wl)          # the per-bucket path against the oracle itself
+    for t in (1, 2, 3):
+        orc.step(t)
+    compare_state(B, orc, 3)
     B.set_grad_clip(1.0)
     with pytest.raises(lamb.LambError) as e:
         B.step_bucket(0, 4)
@@ -470,6 +485,34 @@ def test_cuda_graph_step_equals_eager(lamb):
         assert np.array_equal(E.get_state(k).view(np.uint32), G.get_state(k).view(np.uint32))
     assert torch.equal(E.param_buffer().view(torch.int16), G.param_buffer().view(torch.int16))
     assert G.step_info()["clip"] < 1.0
+    E.close()
+    G.close()
+
+
+def test_cuda_graph_follows_changed_clip_and_loss_scale(lamb):
+    """the pre-step scalars (max_grad_norm, inv_loss_scale) are passed to the graph's
+    kernels by value, so changing them from one non-default value to another must re-capture;
+    eager and graph handles stay bitwise equal while both change every step."""
+    rng = np.random.default_rng(71)
+    tensors = W.random_table(rng, 20, max_numel=20000, p_big=0.2, big=60_000)
+    wl = W.Workload("graphclip", 99, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    E = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=50_000)
+    G = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=50_000, graph=True)
+    for L in (E, G):
+        L.synth_init(spec, wl.seed)
+    settings = [(0.05, 1.0), (0.02, 1.0), (0.02, 0.5), (0.08, 0.25), (0.0, 0.25)]
+    for t, (clip, inv) in enumerate(settings, start=1):
+        for L in (E, G):
+            L.set_grad_clip(clip)
+            L.set_loss_scale(inv)
+            L.synth_grads(spec, wl.seed, 1, t)
+            L.step(t)
+        torch.cuda.synchronize()
+        ie, ig = E.step_info(), G.step_info()
+        assert ie["clip"] == ig["clip"] and ie["grad_norm"] == ig["grad_norm"], (t, ie, ig)
+        for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V):
+            assert np.array_equal(E.get_state(k).view(np.uint32), G.get_state(k).view(np.uint32)), t
     E.close()
     G.close()
 
@@ -576,4 +619,73 @@ def test_copy_engine_schedule_needs_the_flag(lamb):
     L.synth_grads(spec_of(wl), wl.seed, 1, 1)
     L.step(1)
     torch.cuda.synchronize()
+    L.close()
+
+
+def test_checkpoint_commit_protocol(lamb, tmp_path):
+    """saves go to path.tmp.<n> and are renamed only once every rank committed its
+    partition; a failed save leaves the previous checkpoint at `path` intact; a file with a
+    missing commit word (a partition that never completed) is refused by load."""
+    from ckpt_reader import read_checkpoint
+    wl = W.toy()
+    spec = spec_of(wl)
+    path = str(tmp_path / "c.ckpt")
+    L = run_gpu(wl, steps=2)
+    L.checkpoint_save(path, 2)
+    L.checkpoint_wait()
+    assert os.path.exists(path) and not [f for f in os.listdir(tmp_path) if ".tmp." in f]
+    ck = read_checkpoint(path)
+    assert ck["step"] == 2 and ck["world"] == 1 and ck["commit"][0] != 0
+    good = open(path, "rb").read()
+    # a save that fails (its temporary cannot be created: a directory is in the way, which
+    # stops root too) must not touch the previous file
+    L.synth_grads(spec, wl.seed, 1, 3)
+    L.step(3)
+    os.mkdir(path + ".tmp.1")                # the handle's second save writes path.tmp.1
+    L.checkpoint_save(path, 3)
+    with pytest.raises(lamb.LambError, match="open"):
+        L.checkpoint_wait()
+    assert open(path, "rb").read() == good
+    # a missing commit word: refused
+    bad = bytearray(good)
+    off = 64 + 8 * len(wl.tensors)
+    bad[off:off + 8] = bytes(8)
+    bpath = str(tmp_path / "bad.ckpt")
+    open(bpath, "wb").write(bytes(bad))
+    B = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups)
+    with pytest.raises(lamb.LambError, match="incomplete"):
+        B.checkpoint_load(bpath)
+    assert B.checkpoint_load(path) == 2
+    B.close()
+    L.close()
+
+
+def test_set_master_from_host_needs_one_bucket_of_device_memory(lamb):
+    """lamb_set_master from host memory stages bucket by bucket through one
+    bucket-sized device buffer.  175B-slice-3L layout (BASELINE configs[3]'s layer shape,
+    5.4B params, 87 GB of state at D = 1): after create, a ballast leaves less free device
+    memory than a flat_size fp32 temporary (21.7 GB) but more than one bucket (160 MB); the
+    host round trip W = set_master(x) must succeed and read back exactly."""
+    wl = W.slice_175b(3)
+    L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, bucket_cap=wl.cap)
+    n = L.plan.flat_size
+    max_bucket = int(L.plan.buckets[:, 1].max())
+    free, _ = torch.cuda.mem_get_info()
+    keep = 4 * max_bucket + (2 << 30)        # one bucket + 2 GiB of headroom for the runtime
+    ballast = torch.empty(max(0, free - keep), dtype=torch.uint8, device="cuda")
+    assert torch.cuda.mem_get_info()[0] < 4 * n           # a flat fp32 temporary cannot fit
+    x = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    gen = torch.Generator().manual_seed(5)
+    x.copy_(torch.randn(n, generator=gen))
+    mask = torch.zeros(n, dtype=torch.bool)
+    for t, off in zip(wl.tensors, L.plan.tensor_off.tolist()):
+        mask[off:off + t.numel] = True
+    x[~mask] = 0
+    L.set_master(x)
+    w = L.state_buffer(lamb.LAMB_BUF_W)
+    assert torch.equal(w.cpu(), x), "w != the host master (D = 1: the shard is the flat array)"
+    p = L.param_buffer()
+    for lo in (0, n // 2, n - 4096):
+        assert torch.equal(p[lo:lo + 4096].cpu(), x[lo:lo + 4096].bfloat16())
+    del ballast
     L.close()

@@ -83,3 +83,34 @@ def test_hooks_removed_leave_other_models_alone():
         h.remove()
     _fwd(m, torch.randn(2, 4)).backward()       # removed: nothing recorded
     assert r.waits == [] and r.pushes == []
+
+
+def test_gradient_accumulation_pushes_only_the_last_micro_batch():
+    """under gradient accumulation the buckets must be pushed once, by the last
+    micro-batch's backward (no_sync() on the others); a second backward outside no_sync()
+    before step() raises instead of letting the peers reduce a partial gradient."""
+    m = _model()
+    params = list(m.parameters())
+    r = Rec()
+    ov = BucketOverlap(params, [0, 0, 1, 2, 3, 3], 4, push=r.push, wait=r.wait)
+    hooks = ov.install()
+    try:
+        x = torch.randn(5, 4)
+        ov.sync = False                      # what LambOptimizer.no_sync() does
+        _fwd(m, x).backward()
+        _fwd(m, x).backward()
+        assert r.pushes == []
+        ov.sync = True
+        _fwd(m, x).backward()                # the last micro-batch pushes every used bucket
+        assert sorted(r.pushes) == [(0, 1), (1, 1), (2, 1)]
+        with pytest.raises(RuntimeError, match="no_sync"):
+            _fwd(m, x).backward()            # one more backward before step(): refused
+        ov.before_step(1)
+        ov.after_step(1)
+        for p in params:
+            p.grad = None
+        _fwd(m, x).backward()                # the next step works normally again
+        assert sorted(r.pushes[4:]) == [(0, 2), (1, 2), (2, 2)]
+    finally:
+        for h in hooks:
+            h.remove()
