@@ -5,9 +5,15 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
     python bench.py --impl reference      # the CPU oracle arm (bounded sample, host cores)
 
+`--gpus N > 1` without torchrun re-launches itself as N ranks through torch.distributed.run
+(127.0.0.1); under torchrun it runs as the rank the environment names.
+
 Metric (BASELINE.json): LAMB params updated/sec & step ms at 1/2/4/8 B200; % HBM roofline.
 One step = one lamb_step (rows a1-a6 of SURVEY.md §8(a)) over the whole parameter table,
 inputs resident in HBM (state >> L2, so no flush is needed).  Prints ONE JSON line on rank 0.
+The main value is the `--config` workload (default: BASELINE configs[1], GPT 1.3B layout);
+`north_star_curve` adds the north star's scaling-curve layout (175B slice, 3 layers) timed the
+same way after the main handle is freed (`--no-curve` skips it).
 """
 from __future__ import annotations
 
@@ -15,6 +21,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -34,9 +41,10 @@ FALLBACK_HBM_GBS = 6650.0
 NVLINK_PEER_GBS = 770.0
 NVLINK_PULL_GBS = NVLINK_PEER_GBS
 NVLINK_PUSH_GBS = NVLINK_PEER_GBS
+CURVE_CONFIG = "175b_slice_3l"     # north_star: "1->8 GPU step-time scaling curve on the 175B-slice layout"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -49,8 +57,11 @@ def parse():
     ap.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-curve", action="store_true", help="skip the 175B-slice-3L curve point")
+    ap.add_argument("--curve-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample time")
-    return ap.parse_args()
+    ap.add_argument("--cpu-probe", action="store_true", help=argparse.SUPPRESS)  # internal: 1-core leg
+    return ap.parse_args(argv)
 
 
 def peaks():
@@ -62,12 +73,9 @@ def peaks():
 
 
 # ------------------------------------------------------------------ oracle (CPU) timing
-def oracle_sample(wl, seconds: float, max_steps: int | None = None, warmup: int = 0):
-    """Time the CPU oracle's LAMB step on a bounded sample of the workload: the first
-    transformer layer's tensors (or the first tensors up to ~50M params), repeated steps.
-    Returns (params_per_s, ms_per_step, cores, sample description, steps)."""
-    import numpy as np
-    import oracle
+def sample_ids(wl):
+    """The bounded oracle sample: the first transformer layer's tensors (embedding skipped), or
+    the first tensors up to ~60M params."""
     ids, n = [], 0
     for i, t in enumerate(wl.tensors):
         if t.name == "emb":
@@ -76,6 +84,14 @@ def oracle_sample(wl, seconds: float, max_steps: int | None = None, warmup: int 
         n += t.numel
         if n >= 60_000_000 or (t.name.endswith("fc2.b") and n >= 5_000_000):
             break
+    return ids, n
+
+
+def oracle_time(wl, ids, seconds: float, max_steps: int | None = None, warmup: int = 0):
+    """Time the CPU oracle's LAMB step (as it stands) over tensors `ids` of `wl`, repeated steps,
+    grads pre-generated.  Returns (mean ms per step, steps timed)."""
+    import numpy as np
+    import oracle
     wd = {i: oracle.gen_weights(wl.seed, i, wl.tensors[i].init, wl.tensors[i].numel) for i in ids}
     md = {i: np.zeros(wl.tensors[i].numel) for i in ids}
     vd = {i: np.zeros(wl.tensors[i].numel) for i in ids}
@@ -94,10 +110,78 @@ def oracle_sample(wl, seconds: float, max_steps: int | None = None, warmup: int 
             break
         if max_steps is None and sum(times) >= seconds and len(times) >= 2:
             break
-    ms = 1e3 * statistics.mean(times)
+    return 1e3 * statistics.mean(times), len(times)
+
+
+def oracle_sample(wl, seconds: float, max_steps: int | None = None, warmup: int = 0):
+    """Oracle params/s on the bounded sample.  Returns (params_per_s, ms_per_step, cores,
+    sample description, steps)."""
+    import oracle
+    ids, n = sample_ids(wl)
+    ms, k = oracle_time(wl, ids, seconds, max_steps, warmup)
     desc = (f"{wl.name}: tensors {ids[0]}..{ids[-1]} ({n / 1e6:.1f}M params, first layer), "
-            f"{len(times)} LAMB steps in double, grads pre-generated")
-    return n / (ms / 1e3), ms, oracle.num_threads(), desc, len(times)
+            f"{k} LAMB steps in double, grads pre-generated")
+    return n / (ms / 1e3), ms, oracle.num_threads(), desc, k
+
+
+def cpu_model() -> str | None:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_probe(wl, seconds: float) -> dict:
+    """One oracle leg with whatever OpenMP thread count the environment gives: the workload's
+    sample (params/s) and the full toy step (ms).  Used on all cores in-process and on 1 core in a
+    subprocess (OMP_NUM_THREADS=1), so the oracle itself is never modified for the timing."""
+    import oracle
+    v, ms, cores, desc, k = oracle_sample(wl, seconds)
+    toy = W.toy()
+    toy_ms, toy_k = oracle_time(toy, list(range(len(toy.tensors))), min(1.0, seconds / 4), warmup=2)
+    return {"value": v, "ms_per_sample_step": ms, "cores": cores, "sample": desc, "steps": k,
+            "toy_full_step_ms": toy_ms, "toy_steps": toy_k, "threads": oracle.num_threads()}
+
+
+def cpu_leg(wl, seconds: float, threads: int) -> dict:
+    """Run cpu_probe in a fresh process with OMP_NUM_THREADS=threads (torchrun sets 1 for its
+    ranks, and the e2e leg may have pinned this rank to a NUMA node's CPUs)."""
+    try:
+        env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-probe", "--config", wl.name,
+                            "--cpu-seconds", str(seconds)], capture_output=True, text=True,
+                           timeout=900, env=env, cwd=ROOT)
+        if r.returncode == 0:
+            return json.loads(r.stdout.strip().splitlines()[-1])
+        return {"error": r.stderr[-300:]}
+    except Exception as e:  # pragma: no cover
+        return {"error": repr(e)}
+
+
+def cpu_baseline(wl, seconds: float) -> dict:
+    """SURVEY §8(d) 'Oracle timing': the oracle on all host cores and on 1 core; the sample's
+    params/s, the full toy step, and the workload's full step extrapolated from the sample
+    (labelled: the per-element work of LAMB is uniform, the norms are per tensor)."""
+    allc = cpu_leg(wl, seconds, os.cpu_count() or 1)
+    if "value" not in allc:
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "error": allc.get("error")}
+    one = cpu_leg(wl, max(2.0, seconds / 3), 1)
+    out = {"value": allc["value"], "unit": UNIT, "cores": allc["cores"], "kind": "oracle",
+           "sample": allc["sample"], "ms_per_sample_step": allc["ms_per_sample_step"],
+           "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
+           "toy_full_step_ms": allc["toy_full_step_ms"],
+           "full_step_ms": 1e3 * wl.n_params / allc["value"], "extrapolated": True,
+           "extrapolation": f"{wl.name} full step = n_params / sample params/s (sample above)"}
+    if one and "value" in one:
+        out.update({"value_1core": one["value"], "ms_per_sample_step_1core": one["ms_per_sample_step"],
+                    "cores_1core": one["cores"], "toy_full_step_ms_1core": one["toy_full_step_ms"],
+                    "full_step_ms_1core": 1e3 * wl.n_params / one["value"]})
+    else:
+        out["one_core_error"] = one
+    return out
 
 
 def run_reference(args):
@@ -110,7 +194,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl.name, "sample": desc},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -165,6 +250,60 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+class NvlinkCounters:
+    """NVML NVLink data counters of one GPU, summed over its links: bytes transmitted and
+    received.  Tries the per-link byte counters (NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES) and
+    falls back to the throughput counters (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX, KiB).
+    `read()` returns (tx_bytes, rx_bytes) or None when neither is available."""
+    N_LINKS = 18
+
+    def __init__(self, device: int):
+        self.ok, self.field, self.scale = False, None, 1
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv, self.h = nv, nvml_handle(nv, device)
+            cands = []
+            if hasattr(nv, "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES"):
+                cands.append(("COUNT_XMIT/RCV_BYTES", nv.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES,
+                              nv.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, 1))
+            if hasattr(nv, "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX"):
+                cands.append(("THROUGHPUT_DATA_TX/RX (KiB)", nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                              nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024))
+            for name, ftx, frx, scale in cands:
+                self.ftx, self.frx, self.scale, self.field = ftx, frx, scale, name
+                if self._read_raw() is not None:
+                    self.ok = True
+                    break
+        except Exception:
+            self.ok = False
+
+    def _read_raw(self):
+        nv = self.nv
+        req = [(self.ftx, l) for l in range(self.N_LINKS)] + [(self.frx, l) for l in range(self.N_LINKS)]
+        vals = nv.nvmlDeviceGetFieldValues(self.h, req)
+        tx = rx = 0
+        good = 0
+        for k, v in enumerate(vals):
+            if v.nvmlReturn != 0:
+                continue
+            x = int(v.value.ullVal)
+            good += 1
+            if k < self.N_LINKS:
+                tx += x
+            else:
+                rx += x
+        return (tx * self.scale, rx * self.scale) if good else None
+
+    def read(self):
+        if not self.ok:
+            return None
+        try:
+            return self._read_raw()
+        except Exception:
+            return None
+
+
 # ------------------------------------------------------------------ our arm
 def nvml_handle(pynvml, device: int):
     """NVML handle of CUDA device `device` (matched by UUID: CUDA and NVML orders may differ)."""
@@ -194,11 +333,201 @@ def bind_numa_local(device: int):
     return None
 
 
+def self_launch(args) -> int:
+    """`--gpus N > 1` outside torchrun: run this same command as N ranks, one per GPU, through
+    torch.distributed.run on 127.0.0.1 (the driver's launch form).  Rank 0's JSON line goes
+    straight to stdout."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+class Run:
+    """Timing of one workload on this rank: create the handle, synth state/grads in HBM, W
+    warm-up steps, K timed steps bracketed by barrier + synchronize (CUDA events on the launch
+    stream, per-phase events from the library, NVML clocks and NVLink counters around the
+    region), max over ranks."""
+
+    def __init__(self, wl, args, world, rank, local, pg):
+        import torch
+        from paper_2402_15627_b200 import lamb
+        self.wl, self.world, self.rank, self.local, self.pg = wl, world, rank, local, pg
+        self.lamb = lamb
+        self.comm = lamb.LAMB_COMM_FUSED if args.comm == "fused" else lamb.LAMB_COMM_NCCL
+        spec = [(t.init, t.gexp) for t in wl.tensors]
+        self.L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
+                           device=local, comm_mode=self.comm, bucket_cap=wl.cap, timing=not args.graph, pg=pg,
+                           graph=args.graph)
+        self.L.synth_init(spec, wl.seed)
+        self.L.synth_grads(spec, wl.seed, rank + 1, 1)      # PER_RANK gradients, resident in HBM
+        if args.clip > 0:
+            self.L.set_grad_clip(args.clip)
+        self.stream = torch.cuda.current_stream()
+        self.graph = args.graph
+
+    def barrier(self):
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(self, vals):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return np.asarray(vals, dtype=np.float64)
+        tt = torch.tensor(list(vals), dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return tt.cpu().numpy()
+
+    def time(self, K: int, Wm: int, t0: int = 1):
+        import numpy as np
+        import torch
+        L = self.L
+        for t in range(t0, t0 + Wm):
+            L.step(t)
+        self.barrier()
+        if not self.graph:
+            L.timing_begin(K)
+        n0 = L.launch_count()
+        nvc = NvlinkCounters(self.local) if self.world > 1 else None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(self.local) as clk:
+            self.barrier()
+            c0 = nvc.read() if nvc else None
+            e0.record(self.stream)
+            h0 = time.perf_counter()
+            for t in range(t0 + Wm, t0 + Wm + K):
+                L.step(t)
+            host_us = (time.perf_counter() - h0) / K * 1e6   # host enqueue cost per step (async)
+            e1.record(self.stream)
+            torch.cuda.synchronize()
+            c1 = nvc.read() if nvc else None
+        self.barrier()
+        self.t_next = t0 + Wm + K
+        self.launches = L.launch_count() - n0
+        ms_local = e0.elapsed_time(e1) / K
+        if self.graph:   # no per-phase events inside a graph: attribute the step to the passes by bytes
+            ph = np.zeros(6)
+            ph[1] = ph[4] = ms_local / 2
+        else:
+            ph = L.timing_read().mean(axis=0)       # [K][6] ms per phase, events on the launch stream
+        m = self.max_over_ranks([ms_local] + list(ph))
+        self.ms, self.ph = float(m[0]), m[1:]
+        self.host_us, self.clocks = host_us, clk.summary()
+        self.nvlink_meas = None
+        if nvc is not None:
+            if c0 is not None and c1 is not None:
+                tx, rx = (c1[0] - c0[0]) / K, (c1[1] - c0[1]) / K
+                mm = self.max_over_ranks([tx, rx, -tx, -rx])
+                self.nvlink_meas = {"field": nvc.field, "tx_bytes_per_step_rank0": tx,
+                                    "rx_bytes_per_step_rank0": rx,
+                                    "tx_bytes_per_step_max": float(mm[0]), "rx_bytes_per_step_max": float(mm[1]),
+                                    "tx_bytes_per_step_min": float(-mm[2]), "rx_bytes_per_step_min": float(-mm[3])}
+            else:
+                self.max_over_ranks([0, 0, 0, 0])
+                self.nvlink_meas = {"field": None, "note": "NVML NVLink byte counters unavailable"}
+
+    def roofline(self, args):
+        """Algorithmic-byte roofline of the dominant pass."""
+        L, D = self.L, self.world
+        hbm, hbm_src = peaks()
+        owned = int(sum(s[3] for s in L.plan.segments.tolist()))   # tensor elements this rank owns
+        fused = D > 1 and self.comm == self.lamb.LAMB_COMM_FUSED
+        n_flat = int(L.plan.flat_size)
+        # local HBM bytes per launch: own state (w r, m rw, v rw = 20 B) + gradients: D = 1 reads its
+        # bf16 grads (2 B); FUSED reads its whole flat grad buffer once across all D readers (2 B x
+        # flat / owned per element); NCCL mode reads the fp32 reduced shard (4 B)
+        grad_b = 2 * owned if D == 1 else (2 * n_flat if fused else 4 * owned)
+        bytes_a = 20 * owned + grad_b
+        bytes_b = 16 * owned + (2 * n_flat if fused else 2 * owned)   # m r, v r, w rw + params written
+        nvl_in = 2 * owned * (D - 1) if fused else 0                  # NVLink in per GPU per pass
+        t_a, t_b = float(self.ph[1]), float(self.ph[4])
+        ms = self.ms
+
+        def pass_roof(name, nbytes, t, nvl_peak, nvl):
+            hbm_gbps = nbytes / (t / 1e3) / 1e9
+            out = {"kernel": name, "ms": t, "bytes": nbytes, "GBps": hbm_gbps, "hbm_frac": hbm_gbps / hbm}
+            if nvl:
+                nvl_gbps = nvl / (t / 1e3) / 1e9
+                out.update({"nvlink_in_bytes": nvl, "nvlink_GBps": nvl_gbps, "nvlink_peak": nvl_peak,
+                            "nvlink_frac": nvl_gbps / nvl_peak})
+            # the binding resource: the one whose bytes need the longer time at its peak
+            out["bound"] = "nvlink" if nvl and nvl / nvl_peak > nbytes / hbm else "hbm"
+            return out
+
+        if self.graph:
+            # no per-kernel events inside a replayed graph: the whole step against its HBM bytes
+            ra = rb = dom = pass_roof("step(graph)", bytes_a + bytes_b, ms, NVLINK_PULL_GBS, 0)
+        else:
+            ra = pass_roof("pass_a", bytes_a, t_a, NVLINK_PULL_GBS, nvl_in)
+            rb = pass_roof("pass_b", bytes_b, t_b, NVLINK_PUSH_GBS, nvl_in)
+            dom = ra if t_a >= t_b else rb
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            d = json.load(open(tp)).get(f"{self.wl.name}/D{D}/{args.comm if D > 1 else 'fused'}/{dom['kernel']}")
+            traffic = d["bytes"] if d else None
+        if dom["bound"] == "nvlink":
+            roof = {"bound": "nvlink", "kernel": dom["kernel"], "achieved": dom["nvlink_GBps"],
+                    "peak": dom["nvlink_peak"], "unit": "GB/s", "frac": dom["nvlink_frac"],
+                    "traffic": traffic,
+                    "peak_source": "B200_PROFILING.md measured peer copy, 770 GB/s per direction per GPU"}
+        else:
+            roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["GBps"], "peak": hbm,
+                    "unit": "GB/s", "frac": dom["hbm_frac"], "traffic": traffic, "peak_source": hbm_src}
+        roof.update({"algorithmic_bytes_per_launch": dom["bytes"], "launch_ms": dom["ms"],
+                     "pass_a": ra, "pass_b": rb,
+                     "step_compulsory_frac": (owned * 28 / (ms / 1e3) / 1e9) / hbm})
+        if D > 1:
+            # algorithmic NVLink bytes per GPU per step, each direction: peers' grads pulled by this
+            # rank (RS) + peers' params stored into this rank (AG) = 4 B x owned x (D-1) in; the
+            # same amount out (this rank's grads pulled by peers + its params stored into peers)
+            nvl = 2 * owned * (D - 1) * 2 if fused else None
+            roof["nvlink"] = {"bytes_in_per_gpu": nvl, "GBps_step": nvl / (ms / 1e3) / 1e9 if nvl else None,
+                              "peak_per_direction": NVLINK_PEER_GBS,
+                              "frac_step": nvl / (ms / 1e3) / 1e9 / NVLINK_PEER_GBS if nvl else None,
+                              "traffic": self.nvlink_meas}
+            if nvl and self.nvlink_meas and self.nvlink_meas.get("rx_bytes_per_step_rank0") is not None:
+                roof["nvlink"]["measured_over_algorithmic_rx"] = self.nvlink_meas["rx_bytes_per_step_rank0"] / nvl
+                roof["nvlink"]["measured_over_algorithmic_tx"] = self.nvlink_meas["tx_bytes_per_step_rank0"] / nvl
+        return roof
+
+    def close(self):
+        self.L.close()
+
+
+def ranks_seen(world: int) -> int:
+    """Distinct GPUs (device UUIDs) across the ranks of this run."""
+    import torch
+    import torch.distributed as dist
+    u = str(torch.cuda.get_device_properties(torch.cuda.current_device()).uuid)
+    if world == 1:
+        return 1
+    out = [None] * world
+    dist.all_gather_object(out, u)
+    return len(set(out))
+
+
 def main():
     args = parse()
+    if args.cpu_probe:
+        try:   # every host CPU (a parent may have been pinned to one NUMA node)
+            os.sched_setaffinity(0, set(range(os.cpu_count() or 1)))
+        except OSError:
+            pass
+        print(json.dumps(cpu_probe(W.get(args.config), args.cpu_seconds)), flush=True)
+        return 0
     if args.impl == "reference":
         return run_reference(args)
-    import numpy as np
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     import torch
     import torch.distributed as dist
 
@@ -212,57 +541,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist.group.WORLD
+    n_seen = ranks_seen(world)
 
-    from paper_2402_15627_b200 import lamb
     wl = W.get(args.config)
-    spec = [(t.init, t.gexp) for t in wl.tensors]
-    comm = lamb.LAMB_COMM_FUSED if args.comm == "fused" else lamb.LAMB_COMM_NCCL
-    L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
-                  device=local, comm_mode=comm, bucket_cap=wl.cap, timing=not args.graph, pg=pg,
-                  graph=args.graph)
-    L.synth_init(spec, wl.seed)
-    L.synth_grads(spec, wl.seed, rank + 1, 1)      # PER_RANK gradients, resident in HBM
-    if args.clip > 0:
-        L.set_grad_clip(args.clip)
-    stream = torch.cuda.current_stream()
     K, Wm = args.steps, args.warmup
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    for t in range(1, Wm + 1):
-        L.step(t)
-    barrier()
-    if not args.graph:
-        L.timing_begin(K)
-    n0 = L.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        e0.record(stream)
-        h0 = time.perf_counter()
-        for t in range(Wm + 1, Wm + K + 1):
-            L.step(t)
-        host_us = (time.perf_counter() - h0) / K * 1e6   # host enqueue cost per step (async)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    launches = L.launch_count() - n0
-    ms_local = e0.elapsed_time(e1) / K
-    if args.graph:   # no per-phase events inside a graph: attribute the step to the passes by bytes
-        ph_mean = np.zeros(6)
-        ph_mean[1] = ph_mean[4] = ms_local / 2
-    else:
-        ph = L.timing_read()                  # [K][6] ms per phase, events on the launch stream
-        ph_mean = ph.mean(axis=0)
-    ms = ms_local
-    if world > 1:
-        tt = torch.tensor([ms_local] + list(ph_mean), dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt[0])
-        ph_mean = tt[1:].cpu().numpy()
+    R = Run(wl, args, world, rank, local, pg)
+    R.time(K, Wm)
+    L = R.L
 
     # ---------------- e2e: host buffers through lamb_step_host (H2D grads + D2H params in region)
     e2e = None
@@ -273,115 +558,90 @@ def main():
         hg.copy_(L.grad_buffer())
         hp = torch.empty(flat, dtype=torch.bfloat16, pin_memory=True)
         Ke = max(3, min(K, 20))
-        L.step_host(hg, hp, Wm + K + 1)
-        barrier()
+        t = R.t_next
+        L.step_host(hg, hp, t)
+        R.barrier()
         e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e2.record(stream)
-        for t in range(Wm + K + 2, Wm + K + 2 + Ke):
+        e2.record(R.stream)
+        for t in range(t + 1, t + 1 + Ke):
             L.step_host(hg, hp, t)
-        e3.record(stream)
+        e3.record(R.stream)
         torch.cuda.synchronize()
-        ms_e2e = e2.elapsed_time(e3) / Ke
-        if world > 1:
-            tt = torch.tensor([ms_e2e], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms_e2e = float(tt[0])
+        ms_e2e = float(R.max_over_ranks([e2.elapsed_time(e3) / Ke])[0])
         e2e = {"value": wl.n_params / (ms_e2e / 1e3), "unit": UNIT, "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": 2 * flat * world, "d2h_bytes_per_step": 2 * flat * world,
                "steps": Ke, "api": "lamb_step_host (pinned host grads in, params out)",
                "numa_local_cpus": numa_cpus}
+        del hg, hp
+
+    roof = R.roofline(args) if rank == 0 else None
+    main_line = {"ms": R.ms, "ph": R.ph, "launches": R.launches, "host_us": R.host_us, "clocks": R.clocks,
+                 "flat": L.plan.flat_size}
+    R.close()
+    del R, L
+    torch.cuda.empty_cache()
+
+    # ---------------- the north star's scaling-curve layout, timed the same way
+    curve = None
+    if not args.no_curve and args.config != CURVE_CONFIG and not args.graph:
+        wc = W.get(CURVE_CONFIG)
+        free, total = torch.cuda.mem_get_info()
+        need = 4 * wc.n_params + 12 * wc.n_params // world + (1 << 30)
+        ok = torch.tensor([1.0 if free >= need else 0.0], device="cuda")
+        if world > 1:
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if float(ok[0]) > 0:
+            Rc = Run(wc, args, world, rank, local, pg)
+            Rc.time(max(3, args.curve_steps), max(3, min(Wm, 5)))
+            rc = Rc.roofline(args)
+            curve = {"workload": wc.name, "n_params": wc.n_params, "n_tensors": len(wc.tensors),
+                     "value": wc.n_params / (Rc.ms / 1e3), "unit": UNIT, "ms_per_step": Rc.ms,
+                     "steps": max(3, args.curve_steps), "phases_ms": {n: float(x) for n, x in zip(Rc.lamb.PHASES, Rc.ph)},
+                     "roofline": {k: rc[k] for k in ("bound", "kernel", "achieved", "peak", "unit", "frac")},
+                     "nvlink": rc.get("nvlink"), "clocks": Rc.clocks}
+            Rc.close()
+            del Rc
+            torch.cuda.empty_cache()
+        else:
+            curve = {"workload": wc.name, "skipped": f"needs {need / 1e9:.1f} GB free per GPU, "
+                                                     f"rank {rank} has {free / 1e9:.1f}"}
 
     if rank != 0:
-        L.close()
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
-        return
-
-    # ---------------- roofline of the dominant kernel (algorithmic bytes)
-    hbm, hbm_src = peaks()
-    owned = int(sum(s[3] for s in L.plan.segments.tolist()))   # tensor elements this rank owns
-    D = world
-    fused = D > 1 and comm == lamb.LAMB_COMM_FUSED
-    n_flat = int(L.plan.flat_size)
-    # local HBM bytes per launch: own state (w r, m rw, v rw = 20 B) + gradients: D = 1 reads its
-    # bf16 grads (2 B); FUSED reads its whole flat grad buffer once across all D readers (2 B x
-    # flat / owned per element); NCCL mode reads the fp32 reduced shard (4 B)
-    grad_b = 2 * owned if D == 1 else (2 * n_flat if fused else 4 * owned)
-    bytes_a = 20 * owned + grad_b
-    bytes_b = 16 * owned + (2 * n_flat if fused else 2 * owned)   # m r, v r, w rw + params written
-    nvl_in = 2 * owned * (D - 1) if fused else 0                  # NVLink in per GPU per pass
-    t_a, t_b = float(ph_mean[1]), float(ph_mean[4])
-
-    def pass_roof(name, nbytes, ms, nvl_peak):
-        hbm_gbps = nbytes / (ms / 1e3) / 1e9
-        out = {"kernel": name, "ms": ms, "bytes": nbytes, "GBps": hbm_gbps, "hbm_frac": hbm_gbps / hbm}
-        if nvl_in:
-            nvl_gbps = nvl_in / (ms / 1e3) / 1e9
-            out.update({"nvlink_in_bytes": nvl_in, "nvlink_GBps": nvl_gbps, "nvlink_peak": nvl_peak,
-                        "nvlink_frac": nvl_gbps / nvl_peak})
-        # the binding resource: the one whose bytes need the longer time at its peak
-        out["bound"] = "nvlink" if nvl_in and nvl_in / nvl_peak > nbytes / hbm else "hbm"
-        return out
-
-    if args.graph:
-        # no per-kernel events inside a replayed graph: the whole step against its HBM bytes
-        nvl_in = 0
-        ra = rb = dom = pass_roof("step(graph)", bytes_a + bytes_b, ms, NVLINK_PULL_GBS)
-    else:
-        ra = pass_roof("pass_a", bytes_a, t_a, NVLINK_PULL_GBS)
-        rb = pass_roof("pass_b", bytes_b, t_b, NVLINK_PUSH_GBS)
-        dom = ra if t_a >= t_b else rb
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        d = json.load(open(tp)).get(f"{wl.name}/D{D}/{args.comm if D > 1 else 'fused'}/{dom['kernel']}")
-        traffic = d["bytes"] if d else None
-    if dom["bound"] == "nvlink":
-        roof = {"bound": "nvlink", "kernel": dom["kernel"], "achieved": dom["nvlink_GBps"],
-                "peak": dom["nvlink_peak"], "unit": "GB/s", "frac": dom["nvlink_frac"],
-                "traffic": traffic,
-                "peak_source": "B200_PROFILING.md measured peer copy, 770 GB/s per direction per GPU"}
-    else:
-        roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["GBps"], "peak": hbm,
-                "unit": "GB/s", "frac": dom["hbm_frac"], "traffic": traffic, "peak_source": hbm_src}
-    roof.update({"algorithmic_bytes_per_launch": dom["bytes"], "launch_ms": dom["ms"],
-                 "pass_a": ra, "pass_b": rb,
-                 "step_compulsory_frac": (owned * 28 / (ms / 1e3) / 1e9) / hbm})
-    if D > 1:
-        nvl = 2 * owned * (D - 1) * 2   # bytes in per GPU: peers' grads (RS) + peers' params (AG)
-        roof["nvlink"] = {"bytes_in_per_gpu": nvl, "GBps_step": nvl / (ms / 1e3) / 1e9,
-                          "peak_per_direction": NVLINK_PEER_GBS,
-                          "frac_step": nvl / (ms / 1e3) / 1e9 / NVLINK_PEER_GBS}
+        return 0
 
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        v, cms, cores, desc, k = oracle_sample(wl, args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
-               "ms_per_sample_step": cms}
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl, args.cpu_seconds)   # rank 0, after every timed region
 
+    ms = main_line["ms"]
+    from paper_2402_15627_b200 import lamb
     line = {"metric": METRIC, "value": wl.n_params / (ms / 1e3), "unit": UNIT, "n_gpus": world,
             "steps": K, "warmup": Wm, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Philox4x32-10 grads/weights, DESIGN.md §4)",
             "config": {"workload": wl.name, "n_params": wl.n_params, "n_tensors": len(wl.tensors),
-                       "flat_size": L.plan.flat_size, "world_size": world,
+                       "flat_size": main_line["flat"], "world_size": world,
                        "comm": args.comm if world > 1 else "none", "bucket_cap": wl.cap,
                        "prestep_clip": args.clip if args.clip > 0 else None,
                        "cuda_graph": bool(args.graph),
                        "l2": "inputs larger than L2 (fp32 state of the shard >> 126 MB)",
                        "io_dtype": "bf16 grads in / bf16 params out, fp32 master and moments",
                        "parallelism": f"zero2-dp{world}"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "host_enqueue_us_per_step": host_us,
-            "clocks": clk.summary(),
-            "phases_ms": {n: float(x) for n, x in zip(lamb.PHASES, ph_mean)}}
+            "ranks_seen": n_seen,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": main_line["launches"],
+            "host_enqueue_us_per_step": main_line["host_us"],
+            "clocks": main_line["clocks"],
+            "phases_ms": {n: float(x) for n, x in zip(lamb.PHASES, main_line["ph"])},
+            "north_star_curve": curve}
     print(json.dumps(line), flush=True)
-    L.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

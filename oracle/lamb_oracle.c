@@ -164,6 +164,25 @@ void orc_reduce(int64_t n, int32_t D, const double* const* G, double grad_scale,
     }
 }
 
+uint16_t orc_bf16_rne(double x);
+
+/* Variant reduce of SURVEY.md §8(f) NEXT #1 (NVLS, switch-side reduction; reading Z23 in
+ * DESIGN.md): the sum over the D ranks' gradients is formed in fp32 and rounded ONCE to bf16
+ * (round-to-nearest-even) before it is scaled:  g = grad_scale * bf16_rne(sum_j G_j).
+ * Under the input generator the sum is exact in fp32 (H10), so the rounding of the double sum
+ * below is the rounding of the fp32 sum.  ZeRO-2's aggregate, §2 P:695-697. */
+void orc_reduce_bf16sum(int64_t n, int32_t D, const double* const* G, double grad_scale, double* g) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int32_t j = 0; j < D; ++j) s += G[j][i];
+        uint32_t bits = (uint32_t)orc_bf16_rne(s) << 16;
+        float f;
+        memcpy(&f, &bits, 4);
+        g[i] = grad_scale * (double)f;
+    }
+}
+
 /* fp32 -> bf16 round-to-nearest-even of a double first rounded to float (Z15). */
 uint16_t orc_bf16_rne(double x) {
     float f = (float)x;

@@ -871,6 +871,9 @@ static lamb_status graph_step(lamb_ctx* h, cudaStream_t s) {
     }
     CUDA_TRY(h, cudaGraphLaunch(h->graph_exec, s));
     h->launches += h->graph_launches;
+    // the graph's own record of ev_grad_free was captured, not executed on a stream; record it
+    // eagerly after the replay so check_async / lamb_step_host can query and wait on it
+    CUDA_TRY(h, cudaEventRecord(h->ev_grad_free, s));
     return LAMB_OK;
 }
 

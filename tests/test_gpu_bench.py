@@ -21,7 +21,7 @@ def run(*args):
 
 
 def test_bench_line_contract():
-    d = run("--steps", "3", "--warmup", "3", "--no-cpu-baseline")
+    d = run("--steps", "3", "--warmup", "3", "--cpu-seconds", "2", "--curve-steps", "3")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
@@ -33,8 +33,23 @@ def test_bench_line_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    assert d["ranks_seen"] == 1
+    c = d["cpu_baseline"]   # SURVEY §8(d) oracle timing: all cores and 1 core, toy full step, labelled extrapolation
+    assert c["kind"] == "oracle" and c["value"] > 0 and c["cores"] >= 1 and c["cores_1core"] == 1
+    assert c["toy_full_step_ms"] > 0 and c["extrapolated"] is True and c["full_step_ms"] > 0
+    nc = d["north_star_curve"]   # the north star's scaling-curve layout, timed the same way
+    assert nc["workload"] == "175b_slice_3l" and nc["value"] > 0 and 0 < nc["roofline"]["frac"] < 1.2
+
+
+def test_bench_self_launch_two_ranks():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    d = run("--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-curve")
+    assert d["n_gpus"] == 2 and d["ranks_seen"] == 2 and d["config"]["parallelism"] == "zero2-dp2"
+    assert "nvlink" in d["roofline"] and d["roofline"]["nvlink"]["bytes_in_per_gpu"] > 0
 
 
 def test_bench_small_config_and_graph():
     d = run("--config", "toy", "--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--graph")
+    assert d["north_star_curve"] is None   # not timed with --graph
     assert d["config"]["workload"] == "toy" and d["config"]["cuda_graph"] and d["value"] > 0

@@ -176,6 +176,31 @@ def test_H10_reduced_gradient_exact_in_fp32(D):
     assert np.array_equal(g.astype(np.float32).astype(np.float64), g)   # representable in fp32
 
 
+# ---------------------------------------------------------------- H15 NVLS variant reduce (Z23)
+@pytest.mark.parametrize("D", [2, 4, 8])
+def test_H15_bf16sum_variant_matches_torch_cast(D):
+    # library routine: torch sums the bf16 gradients in fp32 (exact under the generator, H10) and
+    # casts the sum to bf16 with its own RNE; the variant oracle must equal that times grad_scale
+    G_ = [oracle.gen_grads(W.BASE_SEED, r + 1, 5, 1, W.GEXP_VECTOR, 40_000) for r in range(D)]
+    ref = torch.stack([torch.from_numpy(x).bfloat16() for x in G_]).float().sum(0).bfloat16().double() / D
+    assert np.array_equal(oracle.reduce_bf16sum(G_, 1.0 / D), ref.numpy())
+    # and it differs from the exact reduce by at most half a bf16 ulp (8 significant bits: 2^-8 relative)
+    exact = oracle.reduce(G_, 1.0 / D)
+    assert np.all(np.abs(oracle.reduce_bf16sum(G_, 1.0 / D) - exact) <= 2.0 ** -8 * np.abs(exact))
+    assert not np.array_equal(oracle.reduce_bf16sum(G_, 1.0 / D), exact)   # the rounding is real
+
+
+def test_H15_bf16sum_special_cases():
+    # a bf16-representable sum is unchanged (D = 1: the generator's values are bf16 numbers)
+    g1 = oracle.gen_grads(W.BASE_SEED, 1, 2, 3, W.GEXP_MATRIX, 10_000)
+    assert np.array_equal(oracle.reduce_bf16sum([g1], 1.0), oracle.reduce([g1], 1.0))
+    # ties round to even: 1 + 2^-8 lies halfway between 1 and 1 + 2^-7 -> 1; 1 + 3*2^-8 -> 1 + 2^-6
+    a = np.array([1.0, 1.0, -1.0, 1.0])
+    b = np.array([2.0 ** -8, 3 * 2.0 ** -8, -(2.0 ** -8), 2.0 ** -8 + 2.0 ** -12])
+    got = oracle.reduce_bf16sum([a, b], 0.5)
+    assert list(got) == [0.5, 0.5 * (1.0 + 2.0 ** -6), -0.5, 0.5 * (1.0 + 2.0 ** -7)]   # last: above the tie
+
+
 # ---------------------------------------------------------------- H8 shard invariance
 def _flat_state(wl, pl):
     n = pl.flat_size
