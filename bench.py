@@ -51,7 +51,7 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="gpt1.3b", choices=list(W.CONFIGS))
-    ap.add_argument("--comm", default="fused", choices=["fused", "nccl"])
+    ap.add_argument("--comm", default="fused", choices=["fused", "nccl", "nvls"])
     ap.add_argument("--clip", type=float, default=0.0,
                     help="enable the NEXT #3 pre-step with this max grad norm (0 = off)")
     ap.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph")
@@ -357,7 +357,7 @@ class Run:
         from paper_2402_15627_b200 import lamb
         self.wl, self.world, self.rank, self.local, self.pg = wl, world, rank, local, pg
         self.lamb = lamb
-        self.comm = lamb.LAMB_COMM_FUSED if args.comm == "fused" else lamb.LAMB_COMM_NCCL
+        self.comm = {"fused": lamb.LAMB_COMM_FUSED, "nccl": lamb.LAMB_COMM_NCCL, "nvls": lamb.LAMB_COMM_NVLS}[args.comm]
         spec = [(t.init, t.gexp) for t in wl.tensors]
         self.L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
                            device=local, comm_mode=self.comm, bucket_cap=wl.cap, timing=not args.graph, pg=pg,
@@ -439,7 +439,10 @@ class Run:
         L, D = self.L, self.world
         hbm, hbm_src = peaks()
         owned = int(sum(s[3] for s in L.plan.segments.tolist()))   # tensor elements this rank owns
-        fused = D > 1 and self.comm == self.lamb.LAMB_COMM_FUSED
+        # FUSED and NVLS touch the same local HBM bytes: own state, plus this rank's whole flat
+        # grad buffer read once (by the D readers / by the switch) and its whole param buffer
+        # written once (by the D writers / by the switch)
+        fused = D > 1 and self.comm in (self.lamb.LAMB_COMM_FUSED, self.lamb.LAMB_COMM_NVLS)
         n_flat = int(L.plan.flat_size)
         # local HBM bytes per launch: own state (w r, m rw, v rw = 20 B) + gradients: D = 1 reads its
         # bf16 grads (2 B); FUSED reads its whole flat grad buffer once across all D readers (2 B x
@@ -447,7 +450,12 @@ class Run:
         grad_b = 2 * owned if D == 1 else (2 * n_flat if fused else 4 * owned)
         bytes_a = 20 * owned + grad_b
         bytes_b = 16 * owned + (2 * n_flat if fused else 2 * owned)   # m r, v r, w rw + params written
-        nvl_in = 2 * owned * (D - 1) if fused else 0                  # NVLink in per GPU per pass
+        # NVLink bytes per GPU per pass in the busier direction: FUSED pulls (A) / pushes (B) the
+        # D-1 peers' slices, 2(D-1) B per owned element each way; NVLS (switch-side reduce /
+        # multicast store) sends this rank's whole grad buffer to the switch (A, out) and receives
+        # every rank's params (B, in): 2 B per flat element
+        nvls = D > 1 and self.comm == self.lamb.LAMB_COMM_NVLS
+        nvl_in = (2 * n_flat if nvls else 2 * owned * (D - 1)) if fused else 0
         t_a, t_b = float(self.ph[1]), float(self.ph[4])
         ms = self.ms
 
@@ -489,7 +497,7 @@ class Run:
             # algorithmic NVLink bytes per GPU per step, each direction: peers' grads pulled by this
             # rank (RS) + peers' params stored into this rank (AG) = 4 B x owned x (D-1) in; the
             # same amount out (this rank's grads pulled by peers + its params stored into peers)
-            nvl = 2 * owned * (D - 1) * 2 if fused else None
+            nvl = (2 * n_flat * 2 if nvls else 2 * owned * (D - 1) * 2) if fused else None
             roof["nvlink"] = {"bytes_in_per_gpu": nvl, "GBps_step": nvl / (ms / 1e3) / 1e9 if nvl else None,
                               "peak_per_direction": NVLINK_PEER_GBS,
                               "frac_step": nvl / (ms / 1e3) / 1e9 / NVLINK_PEER_GBS if nvl else None,
@@ -528,6 +536,11 @@ def main():
         return run_reference(args)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return self_launch(args)
+    # stdout carries exactly ONE line (the JSON result): native libraries that print on fd 1
+    # (e.g. NCCL's version banner on rank 0) are sent to stderr instead
+    out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     import torch
     import torch.distributed as dist
 
@@ -636,7 +649,7 @@ def main():
             "clocks": main_line["clocks"],
             "phases_ms": {n: float(x) for n, x in zip(lamb.PHASES, main_line["ph"])},
             "north_star_curve": curve}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=out, flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -70,6 +70,17 @@ typedef struct {
 #define LAMB_COMM_NCCL 0     /* baseline: NCCL reduce-scatter(fp32)/all-gather(fp64)/all-gather(bf16) */
 #define LAMB_COMM_FUSED 1    /* default: reduce-scatter fused into pass A (NVLink peer loads,
                                 fp32 sum), all-gather fused into pass B (NVLink peer stores) */
+#define LAMB_COMM_NVLS 2     /* opt-in (§2): both
+                                collectives THROUGH the NVSwitch.  Pass A reduce-scatters with
+                                multimem.ld_reduce (the switch adds the D bf16 gradients in fp32
+                                and returns the sum rounded ONCE to bf16: g = grad_scale *
+                                bf16_rne(sum_j G_j), reading Z23 — a documented variant, not the
+                                exact fp32 sum of the other modes), pass B all-gathers with one
+                                multimem.st per chunk.  The flat grad / param buffers are VMM
+                                allocations bound to two multicast objects (file descriptors
+                                exchanged over Unix-domain sockets during lamb_create).  Needs D
+                                distinct multicast-capable GPUs (EUNSUPPORTED otherwise, on every
+                                rank); no pre-step (lamb_step: EUNSUPPORTED), no LAMB_FLAG_CE */
 /* flags */
 #define LAMB_FLAG_TIMING 1   /* record CUDA events around every phase (lamb_timing_*) */
 #define LAMB_FLAG_GRAPH 2    /* lamb_step replays one captured CUDA graph of the whole step
@@ -136,13 +147,13 @@ lamb_status lamb_create(const lamb_tensor* tensors, int64_t n_tensors, const lam
  * lamb_create_with_allgather, on the calling thread, the same number of times on every rank. */
 typedef int (*lamb_allgather_fn)(const void* send, void* recv, size_t bytes, void* user);
 
-/* COLLECTIVE.  lamb_create for LAMB_COMM_FUSED without an NCCL communicator: the table/config
+/* COLLECTIVE.  lamb_create for LAMB_COMM_FUSED (or NVLS) without an NCCL communicator: the table/config
  * hash and the CUDA-IPC handles of every rank's grad/param/sync buffers are exchanged through
  * `allgather` (§3.2 P:312-317 needs only the RS/AG data paths, which FUSED runs in the
  * pass kernels over peer memory; NCCL there serves only as bootstrap).  Ranks may share a
  * device: D processes on fewer GPUs time-slice it, which exercises the D-rank kernels and
  * protocol on any box (tests; not a performance configuration).  Everything else as
- * lamb_create.  EINVAL: allgather NULL, D > 1 with comm_mode != LAMB_COMM_FUSED, the callback
+ * lamb_create.  EINVAL: allgather NULL, D > 1 with comm_mode not FUSED or NVLS, the callback
  * returned non-zero, or the lamb_create conditions. */
 lamb_status lamb_create_with_allgather(const lamb_tensor* tensors, int64_t n_tensors,
                                        const lamb_group* groups, int32_t n_groups,

@@ -56,7 +56,7 @@ def lib():
         L.orc_apply.argtypes = [I64, P, P, D, D]
         L.orc_lamb_tensor_step.argtypes = [I64, P, P, P, P, P, D, D, D, D, D, I32, I32, I64, P]
         L.orc_reduce.argtypes = [I64, I32, P, D, P]
-        L.orc_reduce_bf16sum.argtypes = [I64, I32, P, D, P]
+        L.orc_bf16_neighbors.argtypes = [I64, P, P, P]
         L.orc_bf16_rne.argtypes = [D]
         L.orc_bf16_rne.restype = ctypes.c_uint16
         L.orc_num_threads.restype = I32
@@ -107,13 +107,13 @@ def reduce(G: List[np.ndarray], grad_scale: float) -> np.ndarray:
     return out
 
 
-def reduce_bf16sum(G: List[np.ndarray], grad_scale: float) -> np.ndarray:
-    """NVLS variant (SURVEY §8(f) #1, reading Z23): grad_scale * bf16_rne(sum_j G_j)."""
-    n = G[0].size
-    arr = (ctypes.c_void_p * len(G))(*[_p(g).value for g in G])
-    out = np.empty(n, np.float64)
-    lib().orc_reduce_bf16sum(n, len(G), arr, grad_scale, _p(out))
-    return out
+def bf16_neighbors(x: np.ndarray):
+    """(lo, hi): the bf16 numbers bracketing each x (equal where x is a bf16 number) — the two
+    values the NVSwitch's reduction may return for an exact sum x (reading Z23)."""
+    x = np.ascontiguousarray(x, np.float64)
+    lo, hi = np.empty_like(x), np.empty_like(x)
+    lib().orc_bf16_neighbors(x.size, _p(x), _p(lo), _p(hi))
+    return lo, hi
 
 
 def bf16_rne_bits(x: np.ndarray) -> np.ndarray:
@@ -179,11 +179,8 @@ class OracleRun:
 
     def __init__(self, workload, world_size: int = 1, mode: int = PER_RANK,
                  tensor_ids: Optional[Iterable[int]] = None, grad_scale: Optional[float] = None,
-                 groups=None, bf16_sum: bool = False):
-        """bf16_sum: reduce with the NVLS variant (reduce_bf16sum, reading Z23) instead of the
-        exact fp32 sum (Z11)."""
+                 groups=None):
         self.wl = workload
-        self.bf16_sum = bf16_sum
         self.D = world_size
         self.mode = mode
         self.groups = groups if groups is not None else workload.groups
@@ -207,7 +204,7 @@ class OracleRun:
         G = [gen_grads(self.wl.seed, rank_term(self.mode, j), i, step, ts.gexp, ts.numel) for j in ranks]
         if self.mode == REPLICATED:
             G = G * self.D
-        return (reduce_bf16sum if self.bf16_sum else reduce)(G, f32(self.grad_scale))
+        return reduce(G, f32(self.grad_scale))
 
     def step(self, t: int, max_grad_norm: float = 0.0, inv_loss_scale: float = 1.0) -> dict:
         """One LAMB step.  With the pre-step of SURVEY §8(f) NEXT #3 (reading Z12'):

@@ -289,7 +289,7 @@ extern "C" lamb_status lamb_checkpoint_load(lamb_t h, const char* path, int64_t*
         CUDA_TRY(h, lamb::launch_cast_to_bf16(h->w + p.shard_base[b], h->param + base + (int64_t)p.rank * sl, sl, s));
         ++h->launches;
     }
-    if (p.world > 1 && h->cfg.comm_mode == LAMB_COMM_FUSED) {
+    if (h->peer_mode()) {   // FUSED or NVLS: peers' param buffers are mapped
         // FUSED: every rank's own slices are cast -> barrier -> pull the peers' slices over
         // NVLink -> barrier (no rank rewrites its slices while a peer may still read them)
         uint64_t* flags[LAMB_MAX_RANKS];

@@ -19,6 +19,7 @@ using lamb::Plan;
 using lamb::SegDesc;
 
 struct CheckpointJob;   // checkpoint.cu
+struct NvlsState;       // nvls.cu
 
 struct lamb_plan_ctx {
     Plan plan;
@@ -65,6 +66,17 @@ struct lamb_ctx {
     __nv_bfloat16* peer_grad[LAMB_MAX_RANKS] = {};
     __nv_bfloat16* peer_param[LAMB_MAX_RANKS] = {};
     char* peer_sync[LAMB_MAX_RANKS] = {};
+    // NVLS mode (LAMB_COMM_NVLS): grad / param are VMM allocations bound to multicast objects;
+    // peer_grad / peer_param are fd-imported mappings of the peers' allocations (not CUDA IPC)
+    NvlsState* nvls = nullptr;
+    __nv_bfloat16* mc_grad = nullptr;    // multicast address of the flat grad buffer
+    __nv_bfloat16* mc_param = nullptr;   // multicast address of the flat param buffer
+    // D > 1 with every peer's buffers mapped (FUSED or NVLS): barriers, straddler rows and the
+    // deferred gather go through peer memory
+    bool peer_mode() const {
+        return cfg.world_size > 1 && (cfg.comm_mode == LAMB_COMM_FUSED || cfg.comm_mode == LAMB_COMM_NVLS);
+    }
+    bool nvls_mode() const { return cfg.world_size > 1 && cfg.comm_mode == LAMB_COMM_NVLS; }
     // NCCL (null in FUSED mode created by lamb_create_with_allgather: the step needs no NCCL)
     ncclComm_t comm = nullptr;
     lamb_allgather_fn host_ag = nullptr;   // bootstrap all-gather, set only inside lamb_create_*
@@ -174,6 +186,11 @@ struct DeviceGuard {
 
 // error plumbing shared by the implementation files
 lamb_status lamb_fail(lamb_ctx* h, lamb_status st, const std::string& msg);
+// bootstrap all-gather of lamb_create (NCCL or the caller's host all-gather), lamb_api.cu
+lamb_status lamb_bootstrap_allgather(lamb_ctx* h, const void* mine, void* all, size_t bytes);
+// NVLS mode buffers (nvls.cu): allocate + bind + map (COLLECTIVE, inside lamb_create), release
+lamb_status lamb_nvls_setup(lamb_ctx* h);
+void lamb_nvls_free(lamb_ctx* h);
 #define CUDA_TRY(h, call)                                                                     \
     do {                                                                                      \
         cudaError_t e_ = (call);                                                              \

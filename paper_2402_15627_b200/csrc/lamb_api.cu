@@ -136,6 +136,7 @@ static void free_ctx(lamb_ctx* h) {
     DeviceGuard device_guard_(h->device);
     if (h->ck_stage) cudaFreeHost(h->ck_stage);
     cudaDeviceSynchronize();
+    lamb_nvls_free(h);   // NVLS: VMM grad/param + peer views + multicast (nulls the pointers)
     for (int j = 0; j < h->cfg.world_size && j < LAMB_MAX_RANKS; ++j) {
         // only IPC-opened peer mappings (FUSED mode); other entries alias this rank's buffers
         if (h->peer_grad[j] && h->peer_grad[j] != h->grad) cudaIpcCloseMemHandle(h->peer_grad[j]);
@@ -275,7 +276,7 @@ static lamb_status build_tables(lamb_ctx* h) {
 // Bootstrap exchange: every rank contributes `bytes` bytes, `all` receives D * bytes in rank
 // order.  Through NCCL (device staging) when the handle has a communicator, else through the
 // caller's host all-gather (lamb_create_with_allgather).
-static lamb_status bootstrap_allgather(lamb_ctx* h, const void* mine, void* all, size_t bytes) {
+lamb_status lamb_bootstrap_allgather(lamb_ctx* h, const void* mine, void* all, size_t bytes) {
     const int D = h->cfg.world_size;
     if (h->host_ag) {
         if (h->host_ag(mine, all, bytes, h->host_ag_user) != 0)
@@ -317,7 +318,7 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
         // the per-rank commit records of checkpoints, checkpoint.cu)
         const uint64_t mine[2] = {hv, h->session};
         std::vector<uint64_t> all(2 * (size_t)D);
-        lamb_status st = bootstrap_allgather(h, mine, all.data(), sizeof(mine));
+        lamb_status st = lamb_bootstrap_allgather(h, mine, all.data(), sizeof(mine));
         if (st != LAMB_OK) return st;
         for (int j = 0; j < D; ++j)
             if (all[2 * j] != hv)
@@ -330,22 +331,38 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
         h->peer_param[j] = h->param;
         h->peer_sync[j] = h->sync;
     }
-    if (h->cfg.comm_mode != LAMB_COMM_FUSED) return LAMB_OK;
-    // exchange IPC handles of grad / param / sync (+ the CE staging) in one all-gather
+    if (!h->peer_mode()) return LAMB_OK;
+    if (h->nvls_mode()) {
+        // NVLS: grad / param are multicast-bound VMM allocations, peers mapped by fd (nvls.cu)
+        lamb_status st = lamb_nvls_setup(h);
+        if (st != LAMB_OK) return st;
+    }
+    // exchange IPC handles of grad / param / sync (+ the CE staging) in one all-gather (NVLS:
+    // only the sync buffer travels as a CUDA-IPC handle)
     cudaIpcMemHandle_t mine[4];
-    const int nh = h->ce() ? 4 : 3;
-    CUDA_TRY(h, cudaIpcGetMemHandle(&mine[0], h->grad));
-    CUDA_TRY(h, cudaIpcGetMemHandle(&mine[1], h->param));
-    CUDA_TRY(h, cudaIpcGetMemHandle(&mine[2], h->sync));
-    if (h->ce()) CUDA_TRY(h, cudaIpcGetMemHandle(&mine[3], h->stage));
+    const bool nv = h->nvls_mode();
+    const int nh = nv ? 1 : (h->ce() ? 4 : 3);
+    if (nv) {
+        CUDA_TRY(h, cudaIpcGetMemHandle(&mine[0], h->sync));
+    } else {
+        CUDA_TRY(h, cudaIpcGetMemHandle(&mine[0], h->grad));
+        CUDA_TRY(h, cudaIpcGetMemHandle(&mine[1], h->param));
+        CUDA_TRY(h, cudaIpcGetMemHandle(&mine[2], h->sync));
+        if (h->ce()) CUDA_TRY(h, cudaIpcGetMemHandle(&mine[3], h->stage));
+    }
     std::vector<cudaIpcMemHandle_t> all((size_t)nh * D);
     {
-        lamb_status st = bootstrap_allgather(h, mine, all.data(), sizeof(cudaIpcMemHandle_t) * nh);
+        lamb_status st = lamb_bootstrap_allgather(h, mine, all.data(), sizeof(cudaIpcMemHandle_t) * nh);
         if (st != LAMB_OK) return st;
     }
     for (int j = 0; j < D; ++j) {
         if (j == r) continue;
         void* p = nullptr;
+        if (nv) {
+            CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[j], cudaIpcMemLazyEnablePeerAccess));
+            h->peer_sync[j] = static_cast<char*>(p);
+            continue;
+        }
         CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 0], cudaIpcMemLazyEnablePeerAccess));
         h->peer_grad[j] = static_cast<__nv_bfloat16*>(p);
         CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 1], cudaIpcMemLazyEnablePeerAccess));
@@ -362,7 +379,7 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
     {
         const uint8_t ok = 1;
         std::vector<uint8_t> oks(D);
-        lamb_status st = bootstrap_allgather(h, &ok, oks.data(), 1);
+        lamb_status st = lamb_bootstrap_allgather(h, &ok, oks.data(), 1);
         if (st != LAMB_OK) return st;
     }
     return LAMB_OK;
@@ -386,10 +403,13 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
         if (tensors[i].reserved != 0) return fail(nullptr, LAMB_EINVAL, "reserved must be 0");
     }
     if (cfg->world_size > 1 && !id && !host_ag) return fail(nullptr, LAMB_EINVAL, "unique id required for D > 1");
-    if (cfg->world_size > 1 && host_ag && cfg->comm_mode != LAMB_COMM_FUSED)
-        return fail(nullptr, LAMB_EINVAL, "the host all-gather bootstrap needs LAMB_COMM_FUSED (no NCCL communicator)");
-    if (cfg->world_size > 1 && cfg->comm_mode != LAMB_COMM_NCCL && cfg->comm_mode != LAMB_COMM_FUSED)
-        return fail(nullptr, LAMB_EUNSUPPORTED, "comm_mode not supported in ABI v1");
+    if (cfg->world_size > 1 && host_ag && cfg->comm_mode == LAMB_COMM_NCCL)
+        return fail(nullptr, LAMB_EINVAL, "the host all-gather bootstrap needs LAMB_COMM_FUSED or NVLS (no NCCL communicator)");
+    if (cfg->world_size > 1 && cfg->comm_mode != LAMB_COMM_NCCL && cfg->comm_mode != LAMB_COMM_FUSED &&
+        cfg->comm_mode != LAMB_COMM_NVLS)
+        return fail(nullptr, LAMB_EUNSUPPORTED, "unknown comm_mode");
+    if (cfg->world_size > 1 && cfg->comm_mode == LAMB_COMM_NVLS && (cfg->flags & LAMB_FLAG_CE))
+        return fail(nullptr, LAMB_EUNSUPPORTED, "LAMB_FLAG_CE is a FUSED-mode schedule (not NVLS)");
     if (!(cfg->grad_scale >= 0.f)) return fail(nullptr, LAMB_EINVAL, "grad_scale must be >= 0");
 
     auto* h = new lamb_ctx();
@@ -455,10 +475,12 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
     } while (0)
     const Plan& p = h->plan;
     const int D = cfg->world_size;
-    CUDA_STEP(dalloc(&h->grad, (size_t)p.flat_size));
-    CUDA_STEP(dalloc(&h->param, (size_t)p.flat_size));
-    CUDA_STEP(cudaMemset(h->grad, 0, (size_t)p.flat_size * 2));
-    CUDA_STEP(cudaMemset(h->param, 0, (size_t)p.flat_size * 2));
+    if (!(D > 1 && cfg->comm_mode == LAMB_COMM_NVLS)) {   // NVLS: multicast-bound VMM, setup_comm
+        CUDA_STEP(dalloc(&h->grad, (size_t)p.flat_size));
+        CUDA_STEP(dalloc(&h->param, (size_t)p.flat_size));
+        CUDA_STEP(cudaMemset(h->grad, 0, (size_t)p.flat_size * 2));
+        CUDA_STEP(cudaMemset(h->param, 0, (size_t)p.flat_size * 2));
+    }
     CUDA_STEP(dalloc(&h->w, (size_t)p.shard_size));
     CUDA_STEP(dalloc(&h->m, (size_t)p.shard_size));
     CUDA_STEP(dalloc(&h->v, (size_t)p.shard_size));
@@ -494,7 +516,7 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
     }
     if (D > 1) {
         STEP(setup_comm(h, id));
-        if (cfg->comm_mode == LAMB_COMM_FUSED) {
+        if (h->peer_mode()) {
             CUDA_STEP(cudaStreamCreateWithFlags(&h->x_stream, cudaStreamNonBlocking));
             CUDA_STEP(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
             CUDA_STEP(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
@@ -587,7 +609,8 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     // 0 = every pass sizes a full persistent wave itself
     const int grid_a = h->max_ctas, grid_b = h->max_ctas;
     const int D = h->cfg.world_size, r = h->cfg.rank;
-    const bool fused = D > 1 && h->cfg.comm_mode == LAMB_COMM_FUSED;
+    const bool fused = h->peer_mode();   // FUSED or NVLS: barriers and exchanges through peer memory
+    const bool nvls = h->nvls_mode();
     const bool nccl = D > 1 && h->cfg.comm_mode == LAMB_COMM_NCCL;
     const bool whole = b0 == 0 && b1 == p.n_buckets();
     bool strad = false;   // a bucket in range holds a straddler (identical on every rank)
@@ -629,6 +652,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     memset(&cp, 0, sizeof(cp));
     if (pre) {
         if (!whole) return fail(h, LAMB_EUNSUPPORTED, "the pre-step (clip / loss scale) needs the whole table: use lamb_step");
+        if (nvls) return fail(h, LAMB_EUNSUPPORTED, "the pre-step is not available in NVLS mode");
         if (!h->g32 && D > 1) {   // FUSED + pre-step: the fp32 reduced shard lives here
             CUDA_TRY(h, dalloc(&h->g32, (size_t)p.shard_size));
         }
@@ -686,6 +710,9 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
             } else {
                 LAUNCH(h, launch_pass_a(sp, D, false, grid_a, s));
             }
+        } else if (nvls) {
+            sp.gmc = h->mc_grad;   // reduce-scatter through the switch (reading Z23)
+            LAUNCH(h, launch_pass_a_nvls(sp, grid_a, s));
         } else {
             LAUNCH(h, launch_pass_a(sp, D, false, grid_a, s));
         }
@@ -696,6 +723,11 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
         mark(h, 3, s);
         const bool push = fused && !defer_ag;
         for (int j = 0; j < D; ++j) sp.pdst[j] = push ? h->peer_param[j] : h->param;
+        sp.pmc = h->mc_param;
+        // pass B: FUSED pushes to the D param buffers, NVLS stores once through the switch
+        auto pass_b = [&](const StepParams& q, cudaStream_t st) -> cudaError_t {
+            return (push && nvls) ? launch_pass_b_nvls(q, grid_b, st) : launch_pass_b(q, push ? D : 1, grid_b, st);
+        };
         // Straddler exchange hidden behind pass B (whole-table FUSED step): pass B streams the
         // non-straddler items while a side stream runs barrier + straddler finalize; the
         // straddler items follow once their ratios are final.  Every barrier stays in one
@@ -716,11 +748,11 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
             sb.items = h->items_b;
             sb.item_begin = 0;
             sb.item_end = h->n_items_b_plain;
-            LAUNCH(h, launch_pass_b(sb, D, grid_b, s));
+            LAUNCH(h, pass_b(sb, s));
             CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_join, 0));
             sb.item_begin = h->n_items_b_plain;
             sb.item_end = h->n_items;
-            LAUNCH(h, launch_pass_b(sb, D, grid_b, s));
+            LAUNCH(h, pass_b(sb, s));
         } else {
             if (fused && strad) {
                 // straddler rows travel through peer memory: barrier, then sum in rank order
@@ -734,7 +766,7 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
                 CUDA_TRY(h, cudaStreamWaitEvent(s, h->pre_b_event, 0));
                 if (fused) LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
             }
-            LAUNCH(h, launch_pass_b(sp, push ? D : 1, grid_b, s));
+            LAUNCH(h, pass_b(sp, s));
         }
         mark(h, 5, s);
         if (fused) {
@@ -880,8 +912,8 @@ static lamb_status graph_step(lamb_ctx* h, cudaStream_t s) {
 extern "C" lamb_status lamb_step(lamb_t h, const void* grads, int64_t step, void* stream) {
     if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
     if (step < 1) return fail(h, LAMB_EINVAL, "step must be >= 1");
-    if (grads && h->cfg.world_size > 1 && h->cfg.comm_mode == LAMB_COMM_FUSED)
-        return fail(h, LAMB_EINVAL, "external grads are not allowed in FUSED mode with D > 1");
+    if (grads && h->peer_mode())
+        return fail(h, LAMB_EINVAL, "external grads are not allowed in FUSED / NVLS mode with D > 1");
     if (!h->master_set) return fail(h, LAMB_ESTATE, "lamb_step before lamb_set_master / lamb_synth_init");
     lamb_status st = check_async(h);
     if (st != LAMB_OK) return st;
@@ -925,7 +957,7 @@ extern "C" lamb_status lamb_gather_bucket(lamb_t h, int64_t bucket, void* stream
     DeviceGuard device_guard_(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t base = p.buckets[4 * bucket], sl = p.buckets[4 * bucket + 1] / D;
-    if (h->cfg.comm_mode == LAMB_COMM_FUSED) {
+    if (h->peer_mode()) {
         // pull the peers' slices over NVLink; they were completed before the barrier that
         // ended their lamb_step_bucket, and are not rewritten before this rank's next
         // barrier of this bucket

@@ -504,6 +504,128 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
     }
 }
 
+// ------------------------------------------------------------ pass A, NVLS
+// The reduce-scatter happens inside the NVSwitch: a consumer thread issues
+// multimem.ld_reduce.add.acc::f32.v4.bf16x2 on the multicast address of 8 gradient elements of
+// this rank's slice; the switch reads them from the D ranks' buffers, adds them in fp32 and
+// returns the sum rounded once to bf16 (reading Z23: g = grad_scale * bf16_rne(sum_j G_j)).  m, v,
+// w stream through the TMA ring of pass_a_tma_kernel.  The ld_reduce of the CTA's next item is
+// issued before the consumers wait for this item's state, so the switch round trip overlaps the
+// ring.  Each consumer thread owns 8-element pairs of chunks (16 B requests through the switch).
+constexpr int kMcPairs = kTmaItem / 8 / kTmaConsumers;   // pairs per consumer thread per item
+static_assert(kMcPairs * 8 * kTmaConsumers == kTmaItem, "item size");
+struct TmaStageS {
+    float4 m[kTmaItem / 4], v[kTmaItem / 4], w[kTmaItem / 4];
+};
+__device__ __forceinline__ uint4 mc_ld_reduce_bf16x8(const __nv_bfloat16* p) {
+    uint4 r;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ void mc_fetch(const StepParams& P, int64_t it, int tid, uint4 (&g)[kMcPairs]) {
+    if (it >= P.item_end) return;
+    const Item I = P.items[it];
+    const int npairs = I.n_chunk >> 1;   // items hold a multiple of 8 elements
+#pragma unroll
+    for (int k = 0; k < kMcPairs; ++k) {
+        const int q = tid + k * kTmaConsumers;
+        if (q < npairs) g[k] = mc_ld_reduce_bf16x8(P.gmc + I.flat_off + 8 * (int64_t)q);
+    }
+}
+
+__global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_nvls_kernel(const __grid_constant__ StepParams P) {
+    constexpr int S = kTmaStages;
+    extern __shared__ __align__(128) unsigned char nvls_smem[];
+    TmaStageS* st = reinterpret_cast<TmaStageS*>(nvls_smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(nvls_smem + sizeof(TmaStageS) * S);
+    uint64_t* empty = full + S;
+    __shared__ double red_w[kTmaConsumers / 32], red_u[kTmaConsumers / 32];
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int k = 0; k < S; ++k) {
+            mbar_init(full + k, 1);
+            mbar_init(empty + k, kTmaConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t first = P.item_begin + blockIdx.x, stride = gridDim.x;
+    if (tid >= kTmaConsumers) {
+        if (tid == kTmaConsumers) {
+            int k = 0;
+            uint32_t phase = 0;
+            for (int64_t it = first; it < P.item_end; it += stride) {
+                mbar_wait(empty + k, phase ^ 1);
+                const Item I = P.items[it];
+                const uint32_t nf = (uint32_t)I.n_chunk * 16u;
+                mbar_expect_tx(full + k, 3 * nf);
+                bulk_g2s(st[k].m, P.m + I.shard_off, nf, full + k);
+                bulk_g2s(st[k].v, P.v + I.shard_off, nf, full + k);
+                bulk_g2s(st[k].w, P.w + I.shard_off, nf, full + k);
+                if (++k == S) { k = 0; phase ^= 1; }
+            }
+        }
+        return;
+    }
+    const float gs = P.grad_scale;
+    const int lane = tid & 31, warp = tid >> 5;
+    int k = 0;
+    uint32_t phase = 0;
+    uint4 gcur[kMcPairs];
+    mc_fetch(P, first, tid, gcur);
+    for (int64_t it = first; it < P.item_end; it += stride) {
+        uint4 gnext[kMcPairs];
+        mc_fetch(P, it + stride, tid, gnext);   // next item's switch reduction in flight
+        const Item I = P.items[it];
+        const GroupConst G = P.groups[I.group];
+        const int npairs = I.n_chunk >> 1;
+        mbar_wait(full + k, phase);
+        float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
+        float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
+        float sw = 0.f, su = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < kMcPairs; ++kk) {
+            const int q = tid + kk * kTmaConsumers;
+            if (q < npairs) {
+                const uint4 g = gcur[kk];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = 2 * q + h;
+                    const uint32_t lo = h ? g.z : g.x, hi = h ? g.w : g.y;
+                    float4 m = st[k].m[c], v = st[k].v[c];
+                    const float4 w = st[k].w[c];
+                    chunk_a(make_float4(bf_lo(lo), bf_hi(lo), bf_lo(hi), bf_hi(hi)), m, v, w, gs, G, sw, su);
+                    __stcs(mp + c, m);
+                    __stcs(vp + c, v);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + k);
+        const double dw = warp_sum((double)sw), du = warp_sum((double)su);
+        if (lane == 0) {
+            red_w[warp] = dw;
+            red_u[warp] = du;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
+        if (tid == 0) {
+            double a = 0.0, b = 0.0;
+            for (int q = 0; q < kTmaConsumers / 32; ++q) {
+                a += red_w[q];
+                b += red_u[q];
+            }
+            P.partials[it] = make_double2(a, b);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers));
+        if (++k == S) { k = 0; phase ^= 1; }
+#pragma unroll
+        for (int kk = 0; kk < kMcPairs; ++kk) gcur[kk] = gnext[kk];
+    }
+}
+
 // ------------------------------------------------------------ pass B
 __device__ __forceinline__ uint2 chunk_b(const float4 m, const float4 v, float4& w, float scale,
                                          const GroupConst& G) {
@@ -525,7 +647,14 @@ struct TmaStageB {
     float4 m[kTmaItem / 4], v[kTmaItem / 4], w[kTmaItem / 4];
 };
 
-template <int ND>
+__device__ __forceinline__ void mc_st_b64(__nv_bfloat16* p, uint2 v) {
+    asm volatile("multimem.st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p),
+                 "l"(((uint64_t)v.y << 32) | (uint64_t)v.x) : "memory");
+}
+
+// MC (NVLS mode): the params go out as ONE multimem.st per chunk to the param buffer's multicast
+// address — the NVSwitch fans it out to every rank's buffer (ND is 1: no unicast peer stores).
+template <int ND, bool MC = false>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const __grid_constant__ StepParams P) {
     extern __shared__ __align__(128) unsigned char tma_smem_b[];
     TmaStageB* st = reinterpret_cast<TmaStageB*>(tma_smem_b);
@@ -572,14 +701,18 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const
             float4 w = st[k].w[c];
             const uint2 pb = chunk_b(st[k].m[c], st[k].v[c], w, scale, G);
             __stcs(wp + c, w);
+            if constexpr (MC) {
+                mc_st_b64(P.pmc + I.flat_off + 4 * (int64_t)c, pb);
+            } else {
 #pragma unroll
-            for (int j = 0; j < ND; ++j) __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c, pb);
+                for (int j = 0; j < ND; ++j) __stcs(reinterpret_cast<uint2*>(P.pdst[j] + I.flat_off) + c, pb);
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + k);
         if (++k == kTmaStages) { k = 0; phase ^= 1; }
     }
-    if constexpr (ND > 1) __threadfence_system();   // peer stores visible before the barrier
+    if constexpr (ND > 1 || MC) __threadfence_system();   // peer stores visible before the barrier
 }
 
 // ------------------------------------------------------------ pre-step (NEXT #3)
@@ -1065,12 +1198,26 @@ cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int budget, c
     return cudaErrorInvalidValue;
 }
 
-template <int ND>
+template <int ND, bool MC = false>
 static cudaError_t pass_b_tma(const StepParams& p, int budget, cudaStream_t s) {
     const size_t smem = sizeof(TmaStageB) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
     static std::atomic<uint64_t> attr{0};
-    set_smem_once(attr, (const void*)pass_b_tma_kernel<ND>, smem);
-    pass_b_tma_kernel<ND><<<capped(sm_count(), budget), kTmaConsumers + 32, smem, s>>>(p);
+    set_smem_once(attr, (const void*)pass_b_tma_kernel<ND, MC>, smem);
+    pass_b_tma_kernel<ND, MC><<<capped(sm_count(), budget), kTmaConsumers + 32, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pass_b_nvls(const StepParams& p, int budget, cudaStream_t s) {
+    if (p.item_end <= p.item_begin) return cudaSuccess;
+    return pass_b_tma<1, true>(p, budget, s);
+}
+
+cudaError_t launch_pass_a_nvls(const StepParams& p, int budget, cudaStream_t s) {
+    if (p.item_end <= p.item_begin) return cudaSuccess;
+    const size_t smem = sizeof(TmaStageS) * kTmaStages + 2 * kTmaStages * sizeof(uint64_t);
+    static std::atomic<uint64_t> attr{0};
+    set_smem_once(attr, (const void*)pass_a_nvls_kernel, smem);
+    pass_a_nvls_kernel<<<capped(sm_count(), budget), kTmaConsumers + 32, smem, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -93,6 +93,10 @@ struct StepParams {
     uint64_t gflag_target;
     int* err;
     uint64_t timeout_ns;
+    // NVLS mode (LAMB_COMM_NVLS): multicast addresses of the flat grad and
+    // param buffers (one address reaches the same offset on every rank through the NVSwitch)
+    const __nv_bfloat16* gmc;   // pass A: multimem.ld_reduce (switch-side fp32 sum, bf16 result)
+    __nv_bfloat16* pmc;         // pass B: multimem.st (one store lands in every rank's buffer)
 };
 
 struct FinalizeParams {
@@ -135,6 +139,10 @@ cudaError_t launch_self_check(const Item* items, int64_t n_items, const float* w
 cudaError_t launch_prologue(const GroupTable& t, int n_groups, GroupConst* dst, cudaStream_t s);
 cudaError_t launch_pass_a(const StepParams& p, int nsrc, bool g32, int budget, cudaStream_t s);
 cudaError_t launch_pass_b(const StepParams& p, int ndst, int budget, cudaStream_t s);
+// NVLS mode: pass A reduces the gradients through the switch (p.gmc), pass B stores the params
+// through it (p.pmc)
+cudaError_t launch_pass_a_nvls(const StepParams& p, int budget, cudaStream_t s);
+cudaError_t launch_pass_b_nvls(const StepParams& p, int budget, cudaStream_t s);
 cudaError_t launch_grad_stats(const StepParams& p, int nsrc, bool materialise, int budget, cudaStream_t s);
 cudaError_t launch_clip_finalize(const ClipParams& p, cudaStream_t s);
 cudaError_t launch_clip_combine(const ClipParams& p, cudaStream_t s);

@@ -27,7 +27,7 @@ STATUS_NAMES = ["LAMB_OK", "LAMB_EINVAL", "LAMB_ENOMEM", "LAMB_ECUDA", "LAMB_ENC
 LAMB_MAX_GROUPS = 64
 LAMB_MAX_RANKS = 8
 LAMB_UNIQUE_ID_BYTES = 128
-LAMB_COMM_NCCL, LAMB_COMM_FUSED = 0, 1
+LAMB_COMM_NCCL, LAMB_COMM_FUSED, LAMB_COMM_NVLS = 0, 1, 2
 LAMB_FLAG_TIMING = 1
 LAMB_FLAG_GRAPH = 2
 LAMB_FLAG_CE = 4
@@ -237,7 +237,7 @@ class Lamb:
                           (LAMB_FLAG_CE if ce else 0))
         self.h = _vp()
         if world_size > 1 and bootstrap == "host":
-            # FUSED without an NCCL communicator: IPC handles exchanged over the caller's group
+            # FUSED / NVLS without an NCCL communicator: handles exchanged over the caller's group
             if pg is None:
                 raise ValueError("bootstrap='host' needs a process group")
             ag = _pg_allgather(pg)

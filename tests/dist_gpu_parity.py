@@ -29,6 +29,10 @@ from gpu_common import compare_state, snapshot_w, spec_of  # noqa: E402
 BOOT = "nccl"
 
 
+def orc_run(wl, world, **kw):
+    return oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK, **kw)
+
+
 def _dev():
     return torch.device("cpu") if BOOT == "host" else torch.device("cuda")
 
@@ -51,6 +55,9 @@ def gather_full_w(L, world):
 
 def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, check_all_params=True):
     from paper_2402_15627_b200 import lamb
+    if mode == lamb.LAMB_COMM_NVLS:
+        assert ids is None
+        return nvls_case(name, wl, world, rank, local, mode, steps, cap=cap)
     L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
                   device=local, comm_mode=mode, bucket_cap=cap if cap else wl.cap, pg=dist.group.WORLD,
                   bootstrap=BOOT)
@@ -62,7 +69,7 @@ def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, chec
             L.w_prev = snapshot_w(L, ids)   # per-step update check of the last step
         L.step(t)
     torch.cuda.synchronize()
-    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK, tensor_ids=ids)
+    orc = orc_run(wl, world, tensor_ids=ids)
     for t in range(1, steps + 1):
         orc.step(t)
     worst = compare_state(L, orc, steps, ids=ids, check_params=False)
@@ -90,6 +97,157 @@ def run_case(name, wl, world, rank, local, mode, steps, cap=None, ids=None, chec
               f"max rel err w (|w|>=1e-3)={worst:.2e}", flush=True)
 
 
+def nvls_case(name, wl, world, rank, local, mode, steps, cap=None, stepper="step"):
+    """NVLS mode (reading Z23).  The switch's multimem.ld_reduce returns,
+    per element, ONE of the two bf16 numbers bracketing the exact sum of the D ranks' gradients
+    (stochastic rounding, measured: profiles/r02/nvls_round_D2_stats.txt), so which one is not
+    predictable; what is unique is checked exactly and the rest for validity, step by step:
+      1. every element's reduced gradient, recovered from the GPU's first moment m_t (the two
+         candidates give m values ~2^-8 relative apart), IS one of the two neighbours: the GPU m
+         lies within a few fp32 ulps of the candidate it picked;
+      2. given those choices (all ranks' pieces gathered per tensor), the oracle's double LAMB
+         reproduces w, m, v, the trust ratios and the per-step update within the usual
+         tolerances (compare_state);
+      3. after the last step every rank's param buffer equals bf16_rne(owner's w) everywhere.
+    stepper: "step" (lamb_step), "bucket" (lamb_step_bucket in backward order with deferred
+    gathers), "graph" (LAMB_FLAG_GRAPH replay), "host" (lamb_step_host, params read back from the
+    pinned host buffer)."""
+    from paper_2402_15627_b200 import lamb
+    L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
+                  device=local, comm_mode=mode, bucket_cap=cap if cap else wl.cap, pg=dist.group.WORLD,
+                  bootstrap=BOOT, graph=stepper == "graph")
+    nb = len(L.plan.buckets)
+    if stepper == "host":
+        hg = torch.empty(L.plan.flat_size, dtype=torch.bfloat16).pin_memory()
+        hp = torch.empty(L.plan.flat_size, dtype=torch.bfloat16).pin_memory()
+    spec = spec_of(wl)
+    L.synth_init(spec, wl.seed)
+    orc = orc_run(wl, world)
+    gs = float(np.float32(1.0 / world))
+    segs = L.plan.segments.tolist()
+    m_prev = {(i, toff): np.zeros(ln) for (i, soff, toff, ln) in segs}
+    n_choice = n_up = 0
+    for t in range(1, steps + 1):
+        L.synth_grads(spec, wl.seed, rank + 1, t)
+        L.w_prev = snapshot_w(L)
+        if stepper == "bucket":
+            for b in reversed(range(nb)):
+                L.step_bucket(b, t, defer_ag=True)
+            for b in range(nb):
+                L.gather_bucket(b)
+        elif stepper == "host":
+            hg.copy_(L.grad_buffer())
+            torch.cuda.synchronize()
+            L.step_host(hg, hp, t)
+        else:
+            L.step(t)
+        torch.cuda.synchronize()
+        m_gpu = L.get_state(lamb.LAMB_BUF_M)
+        mine = {}
+        for (i, soff, toff, ln) in segs:
+            ts, grp = wl.tensors[i], wl.groups[wl.tensors[i].group]
+            x = sum(oracle.gen_grads(wl.seed, j + 1, i, t, ts.gexp, ts.numel)[toff:toff + ln] for j in range(world))
+            lo, hi = oracle.bf16_neighbors(x)
+            b1 = oracle.f32(grp.beta1)
+            cand = [b1 * m_prev[(i, toff)] + (1.0 - b1) * (c * gs) for c in (lo, hi)]
+            gm = m_gpu[soff:soff + ln].astype(np.float64)
+            pick = np.abs(gm - cand[1]) < np.abs(gm - cand[0])
+            mc = np.where(pick, cand[1], cand[0])
+            # the kernel's fp32 fma/mul round twice (<= 1 ulp of the terms, which may cancel);
+            # the two candidates lie (1-b1) gs ulp_bf16 apart, ~2^-8 of the gradient term
+            scale = np.abs(b1 * m_prev[(i, toff)]) + np.abs((1.0 - b1) * np.maximum(np.abs(lo), np.abs(hi)) * gs)
+            bad = np.abs(gm - mc) > 4e-7 * scale + 1e-30
+            assert not bad.any(), (f"{name}: step {t} tensor {i}: m[{toff + int(np.argmax(bad))}] is neither "
+                                   f"bf16 neighbour of the exact gradient sum")
+            mine[(i, toff)] = np.where(pick, hi, lo)
+            n_choice += int(np.sum(lo != hi))
+            n_up += int(np.sum(pick & (lo != hi)))
+            m_prev[(i, toff)] = gm
+        pieces = [None] * world
+        dist.all_gather_object(pieces, mine)
+        g_full = {i: np.zeros(ts.numel) for i, ts in enumerate(wl.tensors)}
+        for d in pieces:
+            for (i, toff), g in d.items():
+                g_full[i][toff:toff + len(g)] = g
+        for i in orc.ids:
+            orc.w_prev[i] = orc.w[i].copy()
+            orc.stats[i] = oracle.lamb_tensor_step(orc.w[i], orc.m[i], orc.v[i], g_full[i] * gs,
+                                                   orc.groups[wl.tensors[i].group], t)
+        worst = compare_state(L, orc, t, check_params=False)
+    full = gather_full_w(L, world)
+    got = (hp if stepper == "host" else L.param_buffer()).view(torch.int16).cpu().numpy().view(np.uint16)
+    assert np.array_equal(got, oracle.bf16_rne_bits(full.astype(np.float64))), f"{name}: params != bf16_rne(w)"
+    assert all(v == 0 for v in L.self_check().values()), L.self_check()
+    tot = torch.tensor([n_choice, n_up], dtype=torch.float64, device=_dev())
+    dist.all_reduce(tot)
+    L.close()
+    if rank == 0:
+        print(f"[ok] {name} D={world} NVLS ({stepper}) steps={steps} straddlers={len(L.plan.straddlers)} "
+              f"max rel err w={worst:.2e}; switch rounded {int(tot[0])} inexact sums, "
+              f"{tot[1] / max(tot[0], 1):.3f} of them up", flush=True)
+
+
+def nvls_ckpt_case(world, rank, local, mode):
+    """NVLS checkpoint: the state a D-rank NVLS run saved is restored exactly (bitwise, per tensor)
+    by D ranks with another bucket cap and by one rank (reshard); the reload rebuilds every rank's
+    params as bf16_rne(w).  (The oracle comparison of NVLS steps is nvls_case's.)"""
+    from paper_2402_15627_b200 import lamb
+    rng = np.random.default_rng(88)
+    tensors = W.random_table(rng, 30, max_numel=5000, p_big=0.2, big=30_000)
+    wl = W.Workload("ckn", 71, tensors, W.default_groups(lr=2.0 ** -7))
+    spec = spec_of(wl)
+    path = f"/tmp/lamb_ckpt_nvls_D{world}.bin"
+    mk = lambda D, r, cap, m: lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=D, rank=r,
+                                        device=local, comm_mode=m, bucket_cap=cap, pg=dist.group.WORLD, bootstrap=BOOT)
+
+    def per_tensor(L, D):
+        out = {}
+        for k in (lamb.LAMB_BUF_W, lamb.LAMB_BUF_M, lamb.LAMB_BUF_V):
+            if D > 1:
+                x = torch.from_numpy(L.get_state(k)).to(_dev())
+                xs = [torch.empty_like(x) for _ in range(D)]
+                dist.all_gather(xs, x)
+                xs = [a.cpu().numpy() for a in xs]
+            else:
+                xs = [L.get_state(k)]
+            pl = oracle.plan([t.numel for t in tensors], D, L.plan_cap or 40_000_000)
+            for j in range(D):
+                for (i, soff, toff, ln) in pl.segments[j]:
+                    out.setdefault((k, i), np.zeros(tensors[i].numel, np.float32))[toff:toff + ln] = xs[j][soff:soff + ln]
+        return out
+
+    A = mk(world, rank, 8192, mode)
+    A.plan_cap = 8192
+    A.synth_init(spec, wl.seed)
+    for t in (1, 2):
+        A.synth_grads(spec, wl.seed, rank + 1, t)
+        A.step(t)
+    A.checkpoint_save(path, 2)
+    A.checkpoint_wait()
+    ref = per_tensor(A, world)
+    A.close()
+    dist.barrier()
+    B = mk(world, rank, 5000, mode)
+    B.plan_cap = 5000
+    assert B.checkpoint_load(path) == 2
+    got = per_tensor(B, world)
+    assert all(np.array_equal(got[k].view(np.uint32), ref[k].view(np.uint32)) for k in ref)
+    full = gather_full_w(B, world)
+    p = B.param_buffer().view(torch.int16).cpu().numpy().view(np.uint16)
+    assert np.array_equal(p, oracle.bf16_rne_bits(full.astype(np.float64)))
+    B.close()
+    dist.barrier()
+    if rank == 0:
+        C = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=0)
+        C.plan_cap = 0
+        assert C.checkpoint_load(path) == 2
+        got = per_tensor(C, 1)
+        assert all(np.array_equal(got[k].view(np.uint32), ref[k].view(np.uint32)) for k in ref)
+        C.close()
+        print(f"[ok] checkpoint NVLS D={world} -> D={world} (new cap) -> D=1 reshard, bitwise", flush=True)
+    dist.barrier()
+
+
 def clip_case(world, rank, local, mode):
     """Pre-step at D ranks: the global norm spans every rank's shard; clipping active; then a
     non-finite gradient on one rank makes every rank skip."""
@@ -98,13 +256,24 @@ def clip_case(world, rank, local, mode):
     tensors = W.random_table(rng, 40, max_numel=5000, p_big=0.2, big=40_000)
     wl = W.Workload("clipd", 72, tensors, W.default_groups(lr=2.0 ** -7))
     spec = spec_of(wl)
-    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+    orc = orc_run(wl, world)
     gn1 = np.sqrt(sum(np.sum(orc.grads(i, 1) ** 2) for i in orc.ids))
     max_norm = float(np.float32(0.3 * gn1))
     L = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
                   device=local, comm_mode=mode, bucket_cap=8192, pg=dist.group.WORLD, bootstrap=BOOT)
     L.synth_init(spec, wl.seed)
     L.set_grad_clip(max_norm)
+    if mode == lamb.LAMB_COMM_NVLS:   # documented: no pre-step in NVLS mode (lamb.h)
+        try:
+            L.step(1)
+            raise AssertionError("NVLS accepted the pre-step")
+        except lamb.LambError as e:
+            assert e.status == lamb.LAMB_EUNSUPPORTED, str(e)
+        L.close()
+        dist.barrier()
+        if rank == 0:
+            print(f"[ok] clip D={world} mode={mode}: pre-step rejected (EUNSUPPORTED)", flush=True)
+        return
     for t in (1, 2):
         L.synth_grads(spec, wl.seed, rank + 1, t)
         L.w_prev = snapshot_w(L)
@@ -157,7 +326,7 @@ def bucket_case(world, rank, local, mode):
         assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32)), k
     assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
     # and against the oracle (per-bucket stepping is the exact LAMB step)
-    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+    orc = orc_run(wl, world)
     for t in (1, 2):
         orc.step(t)
     compare_state(B, orc, 2, check_params=False)
@@ -227,7 +396,7 @@ def ckpt_case(world, rank, local, mode):
     A.checkpoint_wait()
     A.close()
     dist.barrier()
-    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+    orc = orc_run(wl, world)
     for t in (1, 2, 3):
         orc.step(t)
     B = mk(world, rank, 5000, dist.group.WORLD)
@@ -245,7 +414,7 @@ def ckpt_case(world, rank, local, mode):
         # generator stream cannot reproduce)
         C = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, bucket_cap=0)
         assert C.checkpoint_load(path) == 2
-        orc2 = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+        orc2 = orc_run(wl, world)
         for t in (1, 2):
             orc2.step(t)
         compare_state(C, orc2, 2)
@@ -258,7 +427,7 @@ def graph_case(world, rank, local, mode):
     """FUSED mode under LAMB_FLAG_GRAPH (barriers with device epochs inside the replayed graph)
     == eager, bitwise."""
     from paper_2402_15627_b200 import lamb
-    if mode != lamb.LAMB_COMM_FUSED:
+    if mode not in (lamb.LAMB_COMM_FUSED, lamb.LAMB_COMM_NVLS):
         return
     rng = np.random.default_rng(107)
     tensors = W.random_table(rng, 30, max_numel=6000, p_big=0.2, big=40_000)
@@ -329,7 +498,7 @@ def ce_case(world, rank, local, mode):
         assert np.array_equal(A.get_state(k).view(np.uint32), B.get_state(k).view(np.uint32)), k
     assert torch.equal(A.param_buffer().view(torch.int16), B.param_buffer().view(torch.int16))
     assert all(v == 0 for v in A.self_check().values()), A.self_check()
-    orc = oracle.OracleRun(wl, world_size=world, mode=oracle.PER_RANK)
+    orc = orc_run(wl, world)
     for t in (1, 2, 3, 4):
         orc.step(t)
     compare_state(A, orc, 4, check_params=False)
@@ -432,7 +601,7 @@ def hide_case(world, rank, local, mode):
     """FUSED: the straddler exchange hidden behind pass B (side stream, straddler items last) ==
     the serial order (LAMB_NO_STRAD_HIDE), bitwise — w, m, v and every param buffer."""
     from paper_2402_15627_b200 import lamb
-    if mode != lamb.LAMB_COMM_FUSED:
+    if mode not in (lamb.LAMB_COMM_FUSED, lamb.LAMB_COMM_NVLS):
         return
     stress = W.stress_tensors(0, 2000)
     wl = W.Workload("hide", 77, stress, W.default_groups())
@@ -465,6 +634,8 @@ def h10_case(world, rank, local, mode):
     or the fused peer-load sum) equals the exact D-rank sum bit-for-bit (the generator's
     values make the fp32 sum exact in any order)."""
     from paper_2402_15627_b200 import lamb
+    if mode == lamb.LAMB_COMM_NVLS:   # the switch returns the bf16-rounded sum (Z23), not an fp32 one
+        return
     rng = np.random.default_rng(109)
     tensors = W.random_table(rng, 25, max_numel=6000, p_big=0.2, big=40_000)
     wl = W.Workload("h10", 76, tensors, W.default_groups(lr=2.0 ** -7))
@@ -494,6 +665,10 @@ def torch_case(world, rank, local, mode):
     (captured) gradients (ZeRO-2 semantics)."""
     from paper_2402_15627_b200 import lamb
     from paper_2402_15627_b200.torch_optim import LambOptimizer
+    if mode == lamb.LAMB_COMM_NVLS:
+        # real-model gradients: their fp32 sum is not exact, so bf16-rounding it (Z23) can differ
+        # from rounding the exact sum by one bf16 ulp — no element-wise oracle at this tolerance
+        return
     torch.manual_seed(0)
     model = torch.nn.Sequential(torch.nn.Linear(64, 300), torch.nn.GELU(), torch.nn.Linear(300, 17)).cuda().bfloat16()
     ordered = [p for _, p in model.named_parameters()]
@@ -593,7 +768,7 @@ def failure_case(world, rank, local, mode):
     except lamb.LambError as e:
         assert e.status == lamb.LAMB_EINVAL and "different" in str(e), str(e)
     dist.barrier()
-    if mode == lamb.LAMB_COMM_FUSED:
+    if mode in (lamb.LAMB_COMM_FUSED, lamb.LAMB_COMM_NVLS):
         L = lamb.Lamb(tensors, wl.groups, world_size=world, rank=rank, device=local, comm_mode=mode,
                       pg=dist.group.WORLD)
         L.synth_init(spec_of(wl), wl.seed)
@@ -616,7 +791,7 @@ def failure_case(world, rank, local, mode):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", default="fused", choices=["fused", "nccl"])
+    ap.add_argument("--mode", default="fused", choices=["fused", "nccl", "nvls"])
     ap.add_argument("--big", action="store_true", help="also run the 1.3B layout (sampled)")
     ap.add_argument("--full", action="store_true",
                     help="only the full-size BASELINE configs: 530B+stress (all stress tensors and "
@@ -629,7 +804,8 @@ def main():
     rank = int(os.environ["RANK"])
     local = int(os.environ["LOCAL_RANK"])
     from paper_2402_15627_b200 import lamb
-    mode = lamb.LAMB_COMM_FUSED if a.mode == "fused" else lamb.LAMB_COMM_NCCL
+    mode = {"fused": lamb.LAMB_COMM_FUSED, "nccl": lamb.LAMB_COMM_NCCL, "nvls": lamb.LAMB_COMM_NVLS}[a.mode]
+
     if a.oversub:
         global BOOT
         BOOT = "host"
@@ -680,8 +856,27 @@ def main():
     run_case("toy10", W.toy(), world, rank, local, mode, 10)
     rng = np.random.default_rng(321)
     tensors = W.random_table(rng, 60, max_numel=4000, p_big=0.15, big=50_000)
-    run_case("ragged", W.Workload("ragged", 50, tensors, W.default_groups(lr=2.0 ** -7)), world, rank,
-             local, mode, 3, cap=8192)
+    ragged = W.Workload("ragged", 50, tensors, W.default_groups(lr=2.0 ** -7))
+    run_case("ragged", ragged, world, rank, local, mode, 3, cap=8192)
+    if mode == lamb.LAMB_COMM_NVLS:
+        # NVLS: the switch's stochastic bf16 rounding makes two handles (different buffers)
+        # differ bitwise, so every schedule is validated against the oracle by nvls_case
+        for st in ("bucket", "graph", "host"):
+            nvls_case(f"ragged-{st}", ragged, world, rank, local, mode, 3, cap=8192, stepper=st)
+        run_case("stress", W.Workload("stress", 51, W.stress_tensors(0, 3000), W.default_groups()), world, rank,
+                 local, mode, 2, cap=100_000)
+        nvls_ckpt_case(world, rank, local, mode)
+        clip_case(world, rank, local, mode)
+        replicated_case(world, rank, local, mode)
+        os.environ["LAMB_BARRIER_TIMEOUT_MS"] = "1500"
+        failure_case(world, rank, local, mode)
+        if a.big:
+            wl = W.gpt_1p3b()
+            nvls_case("gpt1.3b-first-layers", W.Workload("g13", 1, wl.tensors[1:13], wl.groups), world, rank,
+                      local, mode, 1)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     rng = np.random.default_rng(323)
     tensors = [W.TensorSpec(f"x{k}", int(rng.integers(1, 30000)), k % 4, W.INIT_UNIFORM, W.GEXP_MATRIX)
                for k in range(16)]

@@ -1,5 +1,5 @@
-"""Multi-GPU parity (FUSED peer-memory path and the NCCL baseline), launched with torchrun,
-one process per GPU.  Skips when fewer than 2 GPUs are visible."""
+"""Multi-GPU parity (FUSED peer-memory path, the NCCL baseline and the NVLS multicast mode),
+launched with torchrun, one process per GPU.  Skips when fewer than 2 GPUs are visible."""
 import os
 import subprocess
 import sys
@@ -27,6 +27,18 @@ def _torchrun(n, *args, timeout=900):
 @pytest.mark.parametrize("mode", ["fused", "nccl"])
 def test_parity_2gpu(mode):
     _torchrun(2, "--mode", mode)
+
+
+@needs2
+def test_parity_2gpu_nvls():
+    """NVLS mode: reduce-scatter by multimem.ld_reduce, all-gather by
+    multimem.st, against the variant oracle g = grad_scale * bf16_rne(sum_j G_j) (reading Z23)."""
+    _torchrun(2, "--mode", "nvls")
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs >= 4 GPUs")
+def test_parity_4gpu_nvls():
+    _torchrun(4, "--mode", "nvls")
 
 
 @pytest.mark.skipif(NGPU < 4, reason="needs >= 4 GPUs")

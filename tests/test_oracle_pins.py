@@ -176,29 +176,33 @@ def test_H10_reduced_gradient_exact_in_fp32(D):
     assert np.array_equal(g.astype(np.float32).astype(np.float64), g)   # representable in fp32
 
 
-# ---------------------------------------------------------------- H15 NVLS variant reduce (Z23)
+# ---------------------------------------------------------------- H15 bf16 neighbours (Z23, NVLS)
+def _bf16_next_up(x):
+    t = torch.from_numpy(np.asarray(x, np.float64)).bfloat16()
+    return torch.nextafter(t, torch.full_like(t, float("inf"))).double().numpy()
+
+
 @pytest.mark.parametrize("D", [2, 4, 8])
-def test_H15_bf16sum_variant_matches_torch_cast(D):
-    # library routine: torch sums the bf16 gradients in fp32 (exact under the generator, H10) and
-    # casts the sum to bf16 with its own RNE; the variant oracle must equal that times grad_scale
+def test_H15_bf16_neighbors_bracket_the_exact_sum(D):
+    # library routines: torch's RNE cast of the exact sum is one of the two neighbours, and the
+    # neighbours are adjacent bf16 numbers (torch.nextafter on bf16) bracketing the sum
     G_ = [oracle.gen_grads(W.BASE_SEED, r + 1, 5, 1, W.GEXP_VECTOR, 40_000) for r in range(D)]
-    ref = torch.stack([torch.from_numpy(x).bfloat16() for x in G_]).float().sum(0).bfloat16().double() / D
-    assert np.array_equal(oracle.reduce_bf16sum(G_, 1.0 / D), ref.numpy())
-    # and it differs from the exact reduce by at most half a bf16 ulp (8 significant bits: 2^-8 relative)
-    exact = oracle.reduce(G_, 1.0 / D)
-    assert np.all(np.abs(oracle.reduce_bf16sum(G_, 1.0 / D) - exact) <= 2.0 ** -8 * np.abs(exact))
-    assert not np.array_equal(oracle.reduce_bf16sum(G_, 1.0 / D), exact)   # the rounding is real
+    x = oracle.reduce(G_, 1.0)                                   # exact (H10)
+    lo, hi = oracle.bf16_neighbors(x)
+    rne = torch.from_numpy(x).float().bfloat16().double().numpy()
+    assert np.all((rne == lo) | (rne == hi))
+    assert np.all(lo <= x) and np.all(x <= hi)
+    exact = lo == hi
+    assert np.array_equal(lo[exact], x[exact])
+    assert np.array_equal(_bf16_next_up(lo[~exact]), hi[~exact])
+    assert 0 < exact.sum() < x.size                              # both kinds occur
 
 
-def test_H15_bf16sum_special_cases():
-    # a bf16-representable sum is unchanged (D = 1: the generator's values are bf16 numbers)
-    g1 = oracle.gen_grads(W.BASE_SEED, 1, 2, 3, W.GEXP_MATRIX, 10_000)
-    assert np.array_equal(oracle.reduce_bf16sum([g1], 1.0), oracle.reduce([g1], 1.0))
-    # ties round to even: 1 + 2^-8 lies halfway between 1 and 1 + 2^-7 -> 1; 1 + 3*2^-8 -> 1 + 2^-6
-    a = np.array([1.0, 1.0, -1.0, 1.0])
-    b = np.array([2.0 ** -8, 3 * 2.0 ** -8, -(2.0 ** -8), 2.0 ** -8 + 2.0 ** -12])
-    got = oracle.reduce_bf16sum([a, b], 0.5)
-    assert list(got) == [0.5, 0.5 * (1.0 + 2.0 ** -6), -0.5, 0.5 * (1.0 + 2.0 ** -7)]   # last: above the tie
+def test_H15_bf16_neighbors_special_cases():
+    x = np.array([1.0, 1.0 + 2.0 ** -8, -(1.0 + 2.0 ** -8), -1.5, 2.0 ** -126 * (1 + 2.0 ** -10), 0.0])
+    lo, hi = oracle.bf16_neighbors(x)
+    assert list(lo) == [1.0, 1.0, -(1.0 + 2.0 ** -7), -1.5, 2.0 ** -126, 0.0]
+    assert list(hi) == [1.0, 1.0 + 2.0 ** -7, -1.0, -1.5, 2.0 ** -126 * (1 + 2.0 ** -7), 0.0]
 
 
 # ---------------------------------------------------------------- H8 shard invariance

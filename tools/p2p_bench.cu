@@ -6,6 +6,7 @@
 //   tools/p2p_bench <D> <MiB per peer>
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -232,6 +233,83 @@ float run_mixed(int D, size_t bpp, std::vector<char*>& remote, std::vector<char*
     return (float)(bpp * (D - 1)) / (best * 1e-3f) / 1e9f;
 }
 
+// TMA bulk pulls (what pass A's producer does): one CTA per SM, one elected thread streams
+// `chunk`-byte pieces of the peers' blocks into an S-stage shared-memory ring with
+// cp.async.bulk (mbarrier complete_tx); one consumer warp only releases the stages (no compute,
+// no HBM write): the ceiling of the pull pattern itself.  Items go round robin over the peers.
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__global__ void a2a_tma(Ptrs P, int D, int me, size_t bytes_per_peer, int chunk, int S) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)chunk * S);
+    uint64_t* empty = full + S;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < S; ++k) {
+            asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(full + k)), "r"(1));
+            asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(empty + k)), "r"(1));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int np = D - 1;
+    const size_t per_peer = bytes_per_peer / chunk, total = per_peer * np;
+    if (threadIdx.x == 0) {
+        int k = 0;
+        uint32_t ph = 0;
+        for (size_t it = blockIdx.x; it < total; it += gridDim.x) {
+            asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n"
+                         ::"r"(su32(empty + k)), "r"(ph ^ 1) : "memory");
+            const int j = (me + 1 + (int)(it % np)) % D;
+            const char* src = P.src[j] + (size_t)me * bytes_per_peer + (it / np) * chunk;
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(full + k)), "r"(chunk) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(su32(sm + (size_t)k * chunk)), "l"(src), "r"(chunk), "r"(su32(full + k)) : "memory");
+            if (++k == S) { k = 0; ph ^= 1; }
+        }
+    } else if (threadIdx.x == 32) {
+        int k = 0;
+        uint32_t ph = 0;
+        for (size_t it = blockIdx.x; it < total; it += gridDim.x) {
+            asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n"
+                         ::"r"(su32(full + k)), "r"(ph) : "memory");
+            asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(su32(empty + k)) : "memory");
+            if (++k == S) { k = 0; ph ^= 1; }
+        }
+    }
+}
+
+float run_tma(int D, size_t bpp, std::vector<char*>& remote, int sms, int chunk, int S) {
+    const size_t smem = (size_t)chunk * S + 16 * S;
+    std::vector<cudaEvent_t> e0(D), e1(D);
+    for (int g = 0; g < D; ++g) {
+        CK(cudaSetDevice(g));
+        CK(cudaFuncSetAttribute(a2a_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaEventCreate(&e0[g]));
+        CK(cudaEventCreate(&e1[g]));
+    }
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        for (int g = 0; g < D; ++g) { CK(cudaSetDevice(g)); CK(cudaDeviceSynchronize()); }
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            Ptrs P;
+            for (int j = 0; j < D; ++j) P.src[j] = P.dst[j] = remote[j];
+            CK(cudaEventRecord(e0[g]));
+            a2a_tma<<<sms, 64, smem>>>(P, D, g, bpp, chunk, S);
+            CK(cudaEventRecord(e1[g]));
+        }
+        float worst = 0;
+        for (int g = 0; g < D; ++g) {
+            CK(cudaSetDevice(g));
+            CK(cudaEventSynchronize(e1[g]));
+            float ms;
+            CK(cudaEventElapsedTime(&ms, e0[g], e1[g]));
+            worst = ms > worst ? ms : worst;
+        }
+        best = worst < best ? worst : best;
+    }
+    return (float)(bpp * (D - 1)) / (best * 1e-3f) / 1e9f;
+}
+
 int main(int argc, char** argv) {
     const int D = argc > 1 ? atoi(argv[1]) : 2;
     const size_t mib = argc > 2 ? (size_t)atoll(argv[2]) : 512;
@@ -255,6 +333,14 @@ int main(int argc, char** argv) {
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g));
     }
     printf("{\"D\": %d, \"MiB_per_peer\": %zu", D, mib);
+    if (argc > 3 && atoi(argv[3]) == 1) {   // TMA pull sweep only
+        for (int chunk : {8192, 16384, 32768})
+            for (int S : {4, 8, 16, 24})
+                if ((size_t)chunk * S <= 200 * 1024)
+                    printf(", \"tma_pull_c%d_s%d\": %.1f", chunk, S, run_tma(D, bpp, remote, sms, chunk, S));
+        printf("}\n");
+        return 0;
+    }
     for (int mult : {3, 6, 12}) {   // multiples of 3 so every peer gets the same block count
         const int grid = sms * mult;
         printf(", \"pull8_x%d\": %.1f", mult, run<uint2, false>(D, bpp, remote, local, grid));
