@@ -55,8 +55,7 @@ def parse(argv=None):
     ap.add_argument("--clip", type=float, default=0.0,
                     help="enable the NEXT #3 pre-step with this max grad norm (0 = off)")
     ap.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph")
-    ap.add_argument("--pipe", type=int, default=0,
-                    help="LAMB_FLAG_PIPE with this many chunks (pass A of chunk k+1 next to pass B of chunk k)")
+    ap.add_argument("--max-ctas", type=int, default=0, help="cap the persistent grids (lamb_set_max_ctas; 0 = full)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-curve", action="store_true", help="skip the 175B-slice-3L curve point")
@@ -363,16 +362,15 @@ class Run:
         spec = [(t.init, t.gexp) for t in wl.tensors]
         self.L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
                            device=local, comm_mode=self.comm, bucket_cap=wl.cap, timing=not args.graph, pg=pg,
-                           graph=args.graph, pipe=args.pipe > 0 and world > 1)
-        if args.pipe > 0 and world > 1:
-            self.L.set_pipeline_chunks(args.pipe)
+                           graph=args.graph)
+        if args.max_ctas > 0:
+            self.L.set_max_ctas(args.max_ctas)
         self.L.synth_init(spec, wl.seed)
         self.L.synth_grads(spec, wl.seed, rank + 1, 1)      # PER_RANK gradients, resident in HBM
         if args.clip > 0:
             self.L.set_grad_clip(args.clip)
         self.stream = torch.cuda.current_stream()
         self.graph = args.graph
-        self.whole_step = args.graph or (args.pipe > 0 and world > 1)   # no per-pass attribution
 
     def barrier(self):
         import torch
@@ -421,9 +419,6 @@ class Run:
         if self.graph:   # no per-phase events inside a graph: attribute the step to the passes by bytes
             ph = np.zeros(6)
             ph[1] = ph[4] = ms_local / 2
-        elif self.whole_step:   # pipelined: the passes overlap; the library books the pipeline as pass A
-            ph = L.timing_read().mean(axis=0)
-            ph[4] = 0.0
         else:
             ph = L.timing_read().mean(axis=0)       # [K][6] ms per phase, events on the launch stream
         m = self.max_over_ranks([ms_local] + list(ph))
@@ -478,14 +473,9 @@ class Run:
             out["bound"] = "nvlink" if nvl and nvl / nvl_peak > nbytes / hbm else "hbm"
             return out
 
-        if self.whole_step:
-            # no per-kernel events inside a replayed graph / overlapped passes: the whole step
-            # against its HBM bytes and (D > 1) the NVLink bytes of both passes
-            # per direction over the step: FUSED 2 x 2(D-1) B per owned element; NVLS 2 B per flat
-            # element (grads to the switch / params from it) + 2 B per owned element (the other pass)
-            step_nvl = (2 * n_flat + 2 * owned if nvls else 2 * nvl_in) if nvl_in else 0
-            ra = rb = dom = pass_roof("step(graph)" if self.graph else "step(pipelined)", bytes_a + bytes_b, ms,
-                                      NVLINK_PULL_GBS, step_nvl)
+        if self.graph:
+            # no per-kernel events inside a replayed graph: the whole step against its HBM bytes
+            ra = rb = dom = pass_roof("step(graph)", bytes_a + bytes_b, ms, NVLINK_PULL_GBS, 0)
         else:
             ra = pass_roof("pass_a", bytes_a, t_a, NVLINK_PULL_GBS, nvl_in)
             rb = pass_roof("pass_b", bytes_b, t_b, NVLINK_PUSH_GBS, nvl_in)
@@ -652,7 +642,7 @@ def main():
                        "flat_size": main_line["flat"], "world_size": world,
                        "comm": args.comm if world > 1 else "none", "bucket_cap": wl.cap,
                        "prestep_clip": args.clip if args.clip > 0 else None,
-                       "cuda_graph": bool(args.graph), "pipe": args.pipe if world > 1 else 0,
+                       "cuda_graph": bool(args.graph), "max_ctas": args.max_ctas or None,
                        "l2": "inputs larger than L2 (fp32 state of the shard >> 126 MB)",
                        "io_dtype": "bf16 grads in / bf16 params out, fp32 master and moments",
                        "parallelism": f"zero2-dp{world}"},

@@ -88,16 +88,6 @@ typedef struct {
 #define LAMB_FLAG_CE 4       /* FUSED, D > 1: also set up the copy-engine schedule
                                 (lamb_push_grads_bucket / lamb_step_staged /
                                 lamb_wait_params_bucket): a (D-1) x shard bf16 staging buffer */
-#define LAMB_FLAG_PIPE 8     /* FUSED or NVLS, D > 1: lamb_step runs the table as K chunks of
-                                buckets and overlaps pass A (reduce-scatter) of chunk k+1 with
-                                pass B (all-gather) of chunk k on two streams, each on half the
-                                SMs (§3.2, overlap per model chunk).  In NVLS
-                                mode the two collectives load opposite NVLink directions (the
-                                switch-side reduction sends each GPU's whole grad buffer out, the
-                                multicast store brings every rank's params in), so together they
-                                fill both.  Bitwise equal to the unpipelined step (same per-item
-                                arithmetic and reduction order).  No per-phase timing (the passes
-                                overlap: lamb_timing_read reports the pipeline as pass A) */
 
 typedef struct {
     int32_t world_size;        /* D >= 1, <= LAMB_MAX_RANKS; D = 1 needs no unique id */
@@ -214,10 +204,6 @@ lamb_status lamb_step_bucket(lamb_t h, int64_t bucket, int64_t step, int32_t fla
  * 0 = one full wave, the default) so that a concurrently running compute stream keeps the
  * remaining SMs.  Applies to subsequent lamb_step / lamb_step_bucket calls.  EINVAL: < 0. */
 lamb_status lamb_set_max_ctas(lamb_t h, int32_t max_ctas);
-/* LAMB_FLAG_PIPE: number of chunks K (contiguous bucket ranges of about equal size; clamped to
- * the bucket count; default 4).  Applies to subsequent lamb_step calls; results do not depend
- * on it.  EINVAL: k < 1.  EUNSUPPORTED: handle without LAMB_FLAG_PIPE. */
-lamb_status lamb_set_pipeline_chunks(lamb_t h, int32_t k);
 /* Splits `device`'s SMs into two green contexts (CUDA 12.4+ driver API): lamb_sms SMs (rounded
  * up to the hardware's SM-group granularity; the count is returned in *got_sms) and the rest,
  * and returns one non-blocking stream in each.  Kernels launched into a stream run only on its

@@ -99,12 +99,6 @@ struct lamb_ctx {
     bool host_whole = false;             // LAMB_HOST_WHOLE: whole-step pipeline (A/B timing)
     cudaEvent_t grad_free_event() const { return gf_override ? gf_override : ev_grad_free; }
     int max_ctas = 0;   // SM budget of the streaming passes (0 = one full wave)
-    // LAMB_FLAG_PIPE: chunk k = buckets [pipe_b[k], pipe_b[k+1]); pass B of chunk k runs on
-    // x_stream next to pass A of chunk k+1 on the caller's stream
-    int pipe_chunks = 4;
-    int sms = 0;                               // SM count of the device (half-SM grids)
-    std::vector<cudaEvent_t> ev_pipe;          // [K] chunk k's ratios final (pass B may start)
-    bool pipe() const { return (cfg.flags & LAMB_FLAG_PIPE) && peer_mode(); }
     lamb::GroupConst* d_groups = nullptr;   // per-step group constants (prologue kernel)
     // lamb_self_check: padding ranges and counters (built on first use)
     bool pad_built = false;

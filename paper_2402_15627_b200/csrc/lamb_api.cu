@@ -152,7 +152,7 @@ static void free_ctx(lamb_ctx* h) {
         if (p) cudaFree(p);
     if (h->err_flag_host) cudaFreeHost(h->err_flag_host);
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-    for (auto* vec : {&h->ev_rs, &h->ev_b, &h->tev, &h->ev_hb, &h->ev_gf, &h->ev_pb, &h->ev_db, &h->ev_pipe})
+    for (auto* vec : {&h->ev_rs, &h->ev_b, &h->tev, &h->ev_hb, &h->ev_gf, &h->ev_pb, &h->ev_db})
         for (cudaEvent_t e : *vec) cudaEventDestroy(e);
     for (cudaEvent_t e : {h->ev_start, h->ev_done, h->ev_grad_free, h->ev_h2d, h->ev_params, h->ev_d2h,
                           h->ev_call, h->ev_fork, h->ev_join, h->ev_ce_in, h->ev_ce_pushed, h->ev_ce_params})
@@ -408,8 +408,6 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
     if (cfg->world_size > 1 && cfg->comm_mode != LAMB_COMM_NCCL && cfg->comm_mode != LAMB_COMM_FUSED &&
         cfg->comm_mode != LAMB_COMM_NVLS)
         return fail(nullptr, LAMB_EUNSUPPORTED, "unknown comm_mode");
-    if ((cfg->flags & LAMB_FLAG_PIPE) && (cfg->flags & LAMB_FLAG_GRAPH))
-        return fail(nullptr, LAMB_EUNSUPPORTED, "LAMB_FLAG_PIPE and LAMB_FLAG_GRAPH are exclusive");
     if (cfg->world_size > 1 && cfg->comm_mode == LAMB_COMM_NVLS && (cfg->flags & LAMB_FLAG_CE))
         return fail(nullptr, LAMB_EUNSUPPORTED, "LAMB_FLAG_CE is a FUSED-mode schedule (not NVLS)");
     if (!(cfg->grad_scale >= 0.f)) return fail(nullptr, LAMB_EINVAL, "grad_scale must be >= 0");
@@ -519,7 +517,6 @@ static lamb_status create_impl(const lamb_tensor* tensors, int64_t n_tensors, co
     if (D > 1) {
         STEP(setup_comm(h, id));
         if (h->peer_mode()) {
-            CUDA_STEP(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, cfg->device));
             CUDA_STEP(cudaStreamCreateWithFlags(&h->x_stream, cudaStreamNonBlocking));
             CUDA_STEP(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
             CUDA_STEP(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
@@ -600,85 +597,6 @@ static inline void mark(lamb_ctx* h, int phase, cudaStream_t s) {
         if (e_ != cudaSuccess) return fail(h, LAMB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
         ++(h)->launches;                                                                      \
     } while (0)
-
-// LAMB_FLAG_PIPE (FUSED / NVLS, whole table): chunk k = a contiguous bucket range.  Caller's
-// stream s: pass A(k) -> finalize(k) -> [straddler barrier + finalize(k)] -> event k; x_stream:
-// wait event k -> pass B(k).  Pass A(k+1) (s) and pass B(k) (x_stream) run concurrently, each
-// on half the SMs (persistent grids of ~74 CTAs; the first pass A and the last pass B, which
-// run alone, take the full wave).  Every tensor lives in one bucket, so each chunk's norms and
-// ratios are final after its own pass A + finalize: the arithmetic and reduction order per item
-// are those of the plain step (bitwise equal).  All barriers stay on s, in one global order.
-static lamb_status pipelined(lamb_ctx* h, StepParams sp, FinalizeParams fp, cudaStream_t s) {
-    const Plan& p = h->plan;
-    const int D = h->cfg.world_size, r = h->cfg.rank;
-    const int64_t B = p.n_buckets();
-    const int K = (int)std::max<int64_t>(1, std::min<int64_t>(h->pipe_chunks, B));
-    // chunk edges: bucket ranges of about flat_size / K elements each
-    std::vector<int64_t> edge(1, 0);
-    for (int64_t b = 0, acc = 0; b < B; ++b) {
-        acc += p.buckets[4 * b + 1];
-        if ((int)edge.size() < K && acc * K >= (int64_t)edge.size() * p.flat_size && b + 1 < B) edge.push_back(b + 1);
-    }
-    edge.push_back(B);
-    const int nk = (int)edge.size() - 1;
-    while ((int)h->ev_pipe.size() < nk) {
-        cudaEvent_t e;
-        CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        h->ev_pipe.push_back(e);
-    }
-    uint64_t* flags[LAMB_MAX_RANKS];
-    for (int j = 0; j < D; ++j) flags[j] = h->flags(j);
-    const bool nvls = h->nvls_mode();
-    const int full = h->max_ctas, half = std::max(1, (h->max_ctas > 0 ? h->max_ctas : h->sms) / 2);
-    for (int j = 0; j < D; ++j) {
-        sp.pdst[j] = h->peer_param[j];
-        fp.xrow[j] = h->xbuf(j);
-    }
-    sp.gmc = h->mc_grad;
-    sp.pmc = h->mc_param;
-    for (int k = 0; k < nk; ++k) {
-        const int64_t c0 = edge[k], c1 = edge[k + 1];
-        StepParams a = sp;
-        a.item_begin = h->bucket_item_begin[c0];
-        a.item_end = h->bucket_item_begin[c1];
-        const int ga = k == 0 ? full : half;
-        if (nvls) LAUNCH(h, launch_pass_a_nvls(a, ga, s));
-        else LAUNCH(h, launch_pass_a(a, D, false, ga, s));
-        FinalizeParams f = fp;
-        f.segs = h->segs + h->bucket_seg_begin[c0];
-        f.n_segs = h->bucket_seg_begin[c1] - h->bucket_seg_begin[c0];
-        f.strad_slots = h->strad_slots + h->bucket_strad_begin[c0];
-        f.strad_tensor = h->strad_tensor + h->bucket_strad_begin[c0];
-        f.strad_group = h->strad_group + h->bucket_strad_begin[c0];
-        f.n_local_strad = (int32_t)(h->bucket_strad_begin[c1] - h->bucket_strad_begin[c0]);
-        LAUNCH(h, launch_finalize_segments(f, s));
-        bool strad = false;
-        for (int64_t b = c0; b < c1; ++b) strad = strad || h->bucket_has_strad[b];
-        if (strad) {   // identical on every rank: the barrier sequence stays global
-            LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
-            if (f.n_local_strad > 0) LAUNCH(h, launch_finalize_straddlers(f, s));
-        }
-        CUDA_TRY(h, cudaEventRecord(h->ev_pipe[k], s));
-        CUDA_TRY(h, cudaStreamWaitEvent(h->x_stream, h->ev_pipe[k], 0));
-        StepParams b = sp;
-        b.item_begin = a.item_begin;
-        b.item_end = a.item_end;
-        const int gb = k == nk - 1 ? full : half;
-        if (nvls) LAUNCH(h, launch_pass_b_nvls(b, gb, h->x_stream));
-        else LAUNCH(h, launch_pass_b(b, D, gb, h->x_stream));
-    }
-    CUDA_TRY(h, cudaEventRecord(h->ev_join, h->x_stream));
-    CUDA_TRY(h, cudaStreamWaitEvent(s, h->ev_join, 0));
-    mark(h, 2, s);
-    mark(h, 3, s);
-    mark(h, 4, s);
-    mark(h, 5, s);
-    // params complete everywhere, and every rank finished reading this rank's grads
-    LAUNCH(h, launch_barrier(flags, h->epoch(), r, D, h->err_flag_dev, s, h->barrier_timeout_ns));
-    CUDA_TRY(h, cudaEventRecord(h->grad_free_event(), s));
-    mark(h, 6, s);
-    return LAMB_OK;
-}
 
 // One LAMB step over the buckets [b0, b1) (the whole table for lamb_step, one bucket for
 // lamb_step_bucket).  Every tensor lives in exactly one bucket, so a bucket range is a
@@ -779,8 +697,6 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
             sp.err = h->err_flag_dev;
             sp.timeout_ns = h->barrier_timeout_ns;
         }
-        if (h->pipe() && whole && !pre && !h->staged_now && !defer_ag && !h->pre_b_event)
-            return pipelined(h, sp, fp, s);
         if (pre) {
             // pre-step: global ||g||^2 (FUSED: the reduce-scatter happens here, into g32)
             sp.g32_out = h->g32;
@@ -1437,14 +1353,6 @@ extern "C" lamb_status lamb_self_check(lamb_t h, int64_t counts[5], void* stream
     CUDA_TRY(h, cudaMemcpyAsync(c, h->d_check, sizeof(c), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
     for (int k = 0; k < 5; ++k) counts[k] = (int64_t)c[k];
-    return LAMB_OK;
-}
-
-extern "C" lamb_status lamb_set_pipeline_chunks(lamb_t h, int32_t k) {
-    if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");
-    if (k < 1) return fail(h, LAMB_EINVAL, "k must be >= 1");
-    if (!(h->cfg.flags & LAMB_FLAG_PIPE)) return fail(h, LAMB_EUNSUPPORTED, "handle created without LAMB_FLAG_PIPE");
-    h->pipe_chunks = k;
     return LAMB_OK;
 }
 

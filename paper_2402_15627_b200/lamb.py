@@ -31,7 +31,6 @@ LAMB_COMM_NCCL, LAMB_COMM_FUSED, LAMB_COMM_NVLS = 0, 1, 2
 LAMB_FLAG_TIMING = 1
 LAMB_FLAG_GRAPH = 2
 LAMB_FLAG_CE = 4
-LAMB_FLAG_PIPE = 8
 LAMB_BUCKET_DEFER_AG = 1
 LAMB_BUF_GRAD, LAMB_BUF_PARAM, LAMB_BUF_W, LAMB_BUF_M, LAMB_BUF_V, LAMB_BUF_GSUM = range(6)
 PHASES = ["barrier_in", "pass_a", "finalize", "exchange", "pass_b", "barrier_out"]
@@ -97,7 +96,6 @@ _SIGS = {
     "lamb_step_staged": (_st, [_vp, ctypes.c_int64, _vp]),
     "lamb_wait_params_bucket": (_st, [_vp, ctypes.c_int64, ctypes.c_int64, _vp]),
     "lamb_set_max_ctas": (_st, [_vp, ctypes.c_int32]),
-    "lamb_set_pipeline_chunks": (_st, [_vp, ctypes.c_int32]),
     "lamb_self_check": (_st, [_vp, _vp, _vp]),
     "lamb_sm_partition": (_st, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                 ctypes.POINTER(ctypes.c_int32)]),
@@ -219,7 +217,7 @@ class Lamb:
     def __init__(self, tensors: Sequence[tuple], groups: Sequence, world_size: int = 1, rank: int = 0,
                  device: int = 0, comm_mode: int = LAMB_COMM_FUSED, bucket_cap: int = 0,
                  grad_scale: float = 0.0, timing: bool = False, unique_id: Optional[bytes] = None,
-                 pg=None, graph: bool = False, bootstrap: str = "nccl", ce: bool = False, pipe: bool = False):
+                 pg=None, graph: bool = False, bootstrap: str = "nccl", ce: bool = False):
         import torch
         self.torch = torch
         self.device = device
@@ -236,7 +234,7 @@ class Lamb:
             garr[k].adapt, garr[k].bias_correction = int(get("adapt")), int(get("bias_correction"))
         cfg = lamb_config(world_size, rank, device, comm_mode, bucket_cap, grad_scale,
                           (LAMB_FLAG_TIMING if timing else 0) | (LAMB_FLAG_GRAPH if graph else 0) |
-                          (LAMB_FLAG_CE if ce else 0) | (LAMB_FLAG_PIPE if pipe else 0))
+                          (LAMB_FLAG_CE if ce else 0))
         self.h = _vp()
         if world_size > 1 and bootstrap == "host":
             # FUSED / NVLS without an NCCL communicator: handles exchanged over the caller's group
@@ -310,9 +308,6 @@ class Lamb:
 
     def set_max_ctas(self, max_ctas: int) -> None:
         check(lamb_set_max_ctas(self.h, int(max_ctas)), self.h)
-
-    def set_pipeline_chunks(self, k: int) -> None:
-        check(lamb_set_pipeline_chunks(self.h, int(k)), self.h)
 
     def gather_bucket(self, bucket: int, stream=None) -> None:
         check(lamb_gather_bucket(self.h, int(bucket), self._stream(stream)), self.h)

@@ -111,13 +111,11 @@ def nvls_case(name, wl, world, rank, local, mode, steps, cap=None, stepper="step
       3. after the last step every rank's param buffer equals bf16_rne(owner's w) everywhere.
     stepper: "step" (lamb_step), "bucket" (lamb_step_bucket in backward order with deferred
     gathers), "graph" (LAMB_FLAG_GRAPH replay), "host" (lamb_step_host, params read back from the
-    pinned host buffer), "pipe" (LAMB_FLAG_PIPE: pass A of chunk k+1 next to pass B of chunk k)."""
+    pinned host buffer)."""
     from paper_2402_15627_b200 import lamb
     L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
                   device=local, comm_mode=mode, bucket_cap=cap if cap else wl.cap, pg=dist.group.WORLD,
-                  bootstrap=BOOT, graph=stepper == "graph", pipe=stepper == "pipe")
-    if stepper == "pipe":
-        L.set_pipeline_chunks(3)
+                  bootstrap=BOOT, graph=stepper == "graph")
     nb = len(L.plan.buckets)
     if stepper == "host":
         hg = torch.empty(L.plan.flat_size, dtype=torch.bfloat16).pin_memory()
@@ -631,42 +629,6 @@ def hide_case(world, rank, local, mode):
         print(f"[ok] straddler exchange hidden behind pass B D={world} == serial (bitwise)", flush=True)
 
 
-def pipe_case(world, rank, local, mode):
-    """LAMB_FLAG_PIPE (FUSED): pass A of chunk k+1 overlapped with pass B of chunk k on two
-    streams == the plain step, bitwise (w, m, v and every param buffer), for several chunk
-    counts; the straddler barriers of the chunks stay in one global order."""
-    from paper_2402_15627_b200 import lamb
-    if mode != lamb.LAMB_COMM_FUSED:
-        return
-    rng = np.random.default_rng(111)
-    tensors = W.random_table(rng, 60, max_numel=6000, p_big=0.2, big=50_000) + W.stress_tensors(0, 500)
-    wl = W.Workload("piped", 79, tensors, W.default_groups(lr=2.0 ** -7))
-    spec = spec_of(wl)
-    out = []
-    for k in (0, 1, 3, 7):
-        L = lamb.Lamb([(t.numel, t.group) for t in tensors], wl.groups, world_size=world, rank=rank,
-                      device=local, comm_mode=mode, bucket_cap=15_000, pg=dist.group.WORLD, bootstrap=BOOT,
-                      pipe=k > 0)
-        if k:
-            L.set_pipeline_chunks(k)
-        L.synth_init(spec, wl.seed)
-        for t in (1, 2, 3):
-            L.synth_grads(spec, wl.seed, rank + 1, t)
-            L.step(t)
-        torch.cuda.synchronize()
-        out.append([L.get_state(q).view(np.uint32).copy() for q in (2, 3, 4)] +
-                   [L.param_buffer().view(torch.int16).cpu().numpy().copy()])
-        nb, ns = len(L.plan.buckets), len(L.plan.straddlers)
-        L.close()
-    for o in out[1:]:
-        for a, b in zip(out[0], o):
-            assert np.array_equal(a, b)
-    dist.barrier()
-    if rank == 0:
-        print(f"[ok] pipelined step (K = 1, 3, 7 chunks of {nb} buckets, {ns} straddlers) D={world} == plain "
-              f"(bitwise)", flush=True)
-
-
 def h10_case(world, rank, local, mode):
     """Pin H10 on the GPU: the fp32 reduced gradient (NCCL reduce-scatter of the upcast grads,
     or the fused peer-load sum) equals the exact D-rank sum bit-for-bit (the generator's
@@ -866,7 +828,6 @@ def main():
         graph_case(world, rank, local, mode)
         h10_case(world, rank, local, mode)
         hide_case(world, rank, local, mode)
-        pipe_case(world, rank, local, mode)
         replicated_case(world, rank, local, mode)
         ce_case(world, rank, local, mode)
         ce_rollback_case(world, rank, local, mode)
@@ -900,7 +861,7 @@ def main():
     if mode == lamb.LAMB_COMM_NVLS:
         # NVLS: the switch's stochastic bf16 rounding makes two handles (different buffers)
         # differ bitwise, so every schedule is validated against the oracle by nvls_case
-        for st in ("bucket", "graph", "host", "pipe"):
+        for st in ("bucket", "graph", "host"):
             nvls_case(f"ragged-{st}", ragged, world, rank, local, mode, 3, cap=8192, stepper=st)
         run_case("stress", W.Workload("stress", 51, W.stress_tensors(0, 3000), W.default_groups()), world, rank,
                  local, mode, 2, cap=100_000)
@@ -934,7 +895,6 @@ def main():
     graph_case(world, rank, local, mode)
     h10_case(world, rank, local, mode)
     hide_case(world, rank, local, mode)
-    pipe_case(world, rank, local, mode)
     replicated_case(world, rank, local, mode)
     ce_case(world, rank, local, mode)
     ce_rollback_case(world, rank, local, mode)
