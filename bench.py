@@ -55,6 +55,9 @@ def parse(argv=None):
     ap.add_argument("--clip", type=float, default=0.0,
                     help="enable the NEXT #3 pre-step with this max grad norm (0 = off)")
     ap.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph")
+    ap.add_argument("--pg", default="nccl", choices=["nccl", "gloo"],
+                    help="process group of the harness; gloo also bootstraps the library without NCCL "
+                         "(lamb_create_with_allgather) — e.g. for an ncu capture of rank 0")
     ap.add_argument("--max-ctas", type=int, default=0, help="cap the persistent grids (lamb_set_max_ctas; 0 = full)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -362,7 +365,7 @@ class Run:
         spec = [(t.init, t.gexp) for t in wl.tensors]
         self.L = lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank,
                            device=local, comm_mode=self.comm, bucket_cap=wl.cap, timing=not args.graph, pg=pg,
-                           graph=args.graph)
+                           graph=args.graph, bootstrap="host" if args.pg == "gloo" and world > 1 else "nccl")
         if args.max_ctas > 0:
             self.L.set_max_ctas(args.max_ctas)
         self.L.synth_init(spec, wl.seed)
@@ -385,7 +388,7 @@ class Run:
         import torch.distributed as dist
         if self.world == 1:
             return np.asarray(vals, dtype=np.float64)
-        tt = torch.tensor(list(vals), dtype=torch.float64, device="cuda")
+        tt = torch.tensor(list(vals), dtype=torch.float64, device=_pg_device())
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return tt.cpu().numpy()
 
@@ -508,10 +511,32 @@ class Run:
             if nvl and self.nvlink_meas and self.nvlink_meas.get("rx_bytes_per_step_rank0") is not None:
                 roof["nvlink"]["measured_over_algorithmic_rx"] = self.nvlink_meas["rx_bytes_per_step_rank0"] / nvl
                 roof["nvlink"]["measured_over_algorithmic_tx"] = self.nvlink_meas["tx_bytes_per_step_rank0"] / nvl
+            # per-kernel NVLink bytes measured by ncu (nvlrx/nvltx; one process driving the D GPUs,
+            # tools/nvlink_bytes_1proc.py -> profiles/ncu_nvlink.json): user data and wire bytes of
+            # the busier direction of each pass against the algorithmic bytes
+            tp = os.path.join(ROOT, "profiles", "ncu_nvlink.json")
+            meas = json.load(open(tp)) if os.path.exists(tp) else {}
+            per_pass = {}
+            for name, key, d_user, d_wire in (("pass_a", "pass_a", "nvlink_rx_user_bytes", "nvlink_rx_bytes"),
+                                              ("pass_b", "pass_b", "nvlink_tx_user_bytes", "nvlink_tx_bytes")):
+                e = meas.get(f"{self.wl.name}/D{D}/{args.comm}/{key}")
+                if e and e.get(d_user) and nvl_in:
+                    per_pass[name] = {"algorithmic_bytes": nvl_in, "ncu_user_bytes": e[d_user],
+                                      "ncu_wire_bytes": e[d_wire], "user_over_algorithmic": e[d_user] / nvl_in,
+                                      "wire_over_algorithmic": e[d_wire] / nvl_in,
+                                      "direction": "rx (pulls)" if name == "pass_a" else "tx (pushes)",
+                                      "source": "profiles/ncu_nvlink.json (" + e["source"] + ")"}
+            roof["nvlink"]["ncu_traffic"] = per_pass or None
         return roof
 
     def close(self):
         self.L.close()
+
+
+def _pg_device():
+    """Device of the tensors the harness's collectives use (gloo: host)."""
+    import torch.distributed as dist
+    return "cpu" if dist.is_initialized() and dist.get_backend() == "gloo" else "cuda"
 
 
 def ranks_seen(world: int) -> int:
@@ -555,7 +580,10 @@ def main():
     torch.cuda.set_device(local)
     pg = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.pg == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist.group.WORLD
     n_seen = ranks_seen(world)
 
@@ -603,7 +631,7 @@ def main():
         wc = W.get(CURVE_CONFIG)
         free, total = torch.cuda.mem_get_info()
         need = 4 * wc.n_params + 12 * wc.n_params // world + (1 << 30)
-        ok = torch.tensor([1.0 if free >= need else 0.0], device="cuda")
+        ok = torch.tensor([1.0 if free >= need else 0.0], device=_pg_device())
         if world > 1:
             dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if float(ok[0]) > 0:

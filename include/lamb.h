@@ -152,7 +152,9 @@ typedef int (*lamb_allgather_fn)(const void* send, void* recv, size_t bytes, voi
  * `allgather` (§3.2 P:312-317 needs only the RS/AG data paths, which FUSED runs in the
  * pass kernels over peer memory; NCCL there serves only as bootstrap).  Ranks may share a
  * device: D processes on fewer GPUs time-slice it, which exercises the D-rank kernels and
- * protocol on any box (tests; not a performance configuration).  Everything else as
+ * protocol on any box (tests; not a performance configuration).  Ranks may also live in one
+ * process (one thread per GPU calling this concurrently): peers in the same process are mapped
+ * by peer access instead of CUDA IPC (tools/nvlink_bytes_1proc.py).  Everything else as
  * lamb_create.  EINVAL: allgather NULL, D > 1 with comm_mode not FUSED or NVLS, the callback
  * returned non-zero, or the lamb_create conditions. */
 lamb_status lamb_create_with_allgather(const lamb_tensor* tensors, int64_t n_tensors,

@@ -66,6 +66,7 @@ struct lamb_ctx {
     __nv_bfloat16* peer_grad[LAMB_MAX_RANKS] = {};
     __nv_bfloat16* peer_param[LAMB_MAX_RANKS] = {};
     char* peer_sync[LAMB_MAX_RANKS] = {};
+    uint32_t peer_ipc[LAMB_MAX_RANKS] = {};   // bit k: mapping k (grad, param, sync, stage) is CUDA-IPC-opened
     // NVLS mode (LAMB_COMM_NVLS): grad / param are VMM allocations bound to multicast objects;
     // peer_grad / peer_param are fd-imported mappings of the peers' allocations (not CUDA IPC)
     NvlsState* nvls = nullptr;

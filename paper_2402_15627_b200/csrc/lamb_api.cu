@@ -138,11 +138,12 @@ static void free_ctx(lamb_ctx* h) {
     cudaDeviceSynchronize();
     lamb_nvls_free(h);   // NVLS: VMM grad/param + peer views + multicast (nulls the pointers)
     for (int j = 0; j < h->cfg.world_size && j < LAMB_MAX_RANKS; ++j) {
-        // only IPC-opened peer mappings (FUSED mode); other entries alias this rank's buffers
-        if (h->peer_grad[j] && h->peer_grad[j] != h->grad) cudaIpcCloseMemHandle(h->peer_grad[j]);
-        if (h->peer_param[j] && h->peer_param[j] != h->param) cudaIpcCloseMemHandle(h->peer_param[j]);
-        if (h->peer_sync[j] && h->peer_sync[j] != h->sync) cudaIpcCloseMemHandle(h->peer_sync[j]);
-        if (h->peer_stage[j]) cudaIpcCloseMemHandle(h->peer_stage[j]);
+        // only IPC-opened peer mappings (peers in other processes); other entries alias this
+        // rank's buffers or a same-process peer's own allocation
+        if (h->peer_ipc[j] & 1u) cudaIpcCloseMemHandle(h->peer_grad[j]);
+        if (h->peer_ipc[j] & 2u) cudaIpcCloseMemHandle(h->peer_param[j]);
+        if (h->peer_ipc[j] & 4u) cudaIpcCloseMemHandle(h->peer_sync[j]);
+        if (h->peer_ipc[j] & 8u) cudaIpcCloseMemHandle(h->peer_stage[j]);
     }
     void* ptrs[] = {h->grad, h->param, h->w, h->m, h->v, h->items, h->items_b, h->stage, h->d_item_bucket, h->partials, h->segs, h->scale,
                     h->w_sq, h->u_sq, h->ratio, h->strad_slots, h->strad_tensor, h->strad_group,
@@ -338,41 +339,57 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
         if (st != LAMB_OK) return st;
     }
     // exchange IPC handles of grad / param / sync (+ the CE staging) in one all-gather (NVLS:
-    // only the sync buffer travels as a CUDA-IPC handle)
-    cudaIpcMemHandle_t mine[4];
+    // only the sync buffer travels as a CUDA-IPC handle).  With them travel the process id, the
+    // device and the raw pointers: a peer in THIS process (several ranks driven by one process,
+    // one thread per GPU) is mapped by peer access, not by IPC, which cannot open a handle of
+    // its own process.
+    struct PeerRec {
+        cudaIpcMemHandle_t ipc[4];
+        void* raw[4];
+        int64_t pid;
+        int32_t device, pad;
+    };
+    PeerRec mine;
+    memset(&mine, 0, sizeof(mine));
     const bool nv = h->nvls_mode();
     const int nh = nv ? 1 : (h->ce() ? 4 : 3);
-    if (nv) {
-        CUDA_TRY(h, cudaIpcGetMemHandle(&mine[0], h->sync));
-    } else {
-        CUDA_TRY(h, cudaIpcGetMemHandle(&mine[0], h->grad));
-        CUDA_TRY(h, cudaIpcGetMemHandle(&mine[1], h->param));
-        CUDA_TRY(h, cudaIpcGetMemHandle(&mine[2], h->sync));
-        if (h->ce()) CUDA_TRY(h, cudaIpcGetMemHandle(&mine[3], h->stage));
+    void* bufs[4] = {nv ? (void*)h->sync : (void*)h->grad, (void*)h->param, (void*)h->sync, (void*)h->stage};
+    for (int k = 0; k < nh; ++k) {
+        CUDA_TRY(h, cudaIpcGetMemHandle(&mine.ipc[k], bufs[k]));
+        mine.raw[k] = bufs[k];
     }
-    std::vector<cudaIpcMemHandle_t> all((size_t)nh * D);
+    mine.pid = (int64_t)getpid();
+    mine.device = h->device;
+    std::vector<PeerRec> all((size_t)D);
     {
-        lamb_status st = lamb_bootstrap_allgather(h, mine, all.data(), sizeof(cudaIpcMemHandle_t) * nh);
+        lamb_status st = lamb_bootstrap_allgather(h, &mine, all.data(), sizeof(PeerRec));
         if (st != LAMB_OK) return st;
     }
     for (int j = 0; j < D; ++j) {
         if (j == r) continue;
-        void* p = nullptr;
+        const bool local = all[j].pid == mine.pid;
+        if (local && all[j].device != h->device) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(all[j].device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+            else CUDA_TRY(h, e);
+        }
+        void* q[4] = {nullptr, nullptr, nullptr, nullptr};
+        for (int k = 0; k < nh; ++k) {
+            if (local) {
+                q[k] = all[j].raw[k];
+            } else {
+                CUDA_TRY(h, cudaIpcOpenMemHandle(&q[k], all[j].ipc[k], cudaIpcMemLazyEnablePeerAccess));
+                h->peer_ipc[j] |= 1u << (nv ? 2 : k);   // which mappings free_ctx must close
+            }
+        }
         if (nv) {
-            CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[j], cudaIpcMemLazyEnablePeerAccess));
-            h->peer_sync[j] = static_cast<char*>(p);
+            h->peer_sync[j] = static_cast<char*>(q[0]);
             continue;
         }
-        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 0], cudaIpcMemLazyEnablePeerAccess));
-        h->peer_grad[j] = static_cast<__nv_bfloat16*>(p);
-        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 1], cudaIpcMemLazyEnablePeerAccess));
-        h->peer_param[j] = static_cast<__nv_bfloat16*>(p);
-        CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 2], cudaIpcMemLazyEnablePeerAccess));
-        h->peer_sync[j] = static_cast<char*>(p);
-        if (h->ce()) {
-            CUDA_TRY(h, cudaIpcOpenMemHandle(&p, all[nh * j + 3], cudaIpcMemLazyEnablePeerAccess));
-            h->peer_stage[j] = static_cast<__nv_bfloat16*>(p);
-        }
+        h->peer_grad[j] = static_cast<__nv_bfloat16*>(q[0]);
+        h->peer_param[j] = static_cast<__nv_bfloat16*>(q[1]);
+        h->peer_sync[j] = static_cast<char*>(q[2]);
+        if (h->ce()) h->peer_stage[j] = static_cast<__nv_bfloat16*>(q[3]);
     }
     // make sure every rank has mapped everything before the first step
     CUDA_TRY(h, cudaDeviceSynchronize());
