@@ -29,6 +29,9 @@
 
 #include "../../include/lamb.h"
 #include "../../include/lamb_synth.h"
+#ifdef LAMB_DEBUG
+#include "../../include/lamb_debug.h"
+#endif
 #include "lamb_kernels.cuh"
 #include "planner.hpp"
 #include "synth.cuh"
@@ -646,8 +649,14 @@ static lamb_status step_impl(lamb_ctx* h, const void* grads, int64_t t, cudaStre
     sp.partials = h->partials;
     sp.scale = h->scale;
     sp.groups = h->d_groups;
+    sp.shard_elems = p.shard_size;   // extents for the LAMB_DEBUG build's bounds checks
+    sp.flat_elems = p.flat_size;
+    sp.n_items = h->n_items;
+    sp.n_tensors = (int32_t)p.n_tensors();
     FinalizeParams fp;
     memset(&fp, 0, sizeof(fp));
+    fp.n_items = h->n_items;
+    fp.n_tensors = (int32_t)p.n_tensors();
     fp.segs = h->segs + h->bucket_seg_begin[b0];
     fp.n_segs = h->bucket_seg_begin[b1] - h->bucket_seg_begin[b0];
     fp.partials = h->partials;
@@ -1372,6 +1381,22 @@ extern "C" lamb_status lamb_self_check(lamb_t h, int64_t counts[5], void* stream
     for (int k = 0; k < 5; ++k) counts[k] = (int64_t)c[k];
     return LAMB_OK;
 }
+
+#ifdef LAMB_DEBUG
+extern "C" lamb_status lamb_debug_corrupt_item(lamb_t h, int64_t item, int64_t flat_off) {
+    if (!h || item < 0 || item >= h->n_items) return fail(h, LAMB_EINVAL, "item out of range");
+    DeviceGuard device_guard_(h->device);
+    CUDA_TRY(h, cudaDeviceSynchronize());
+    for (Item* tab : {h->items, h->items_b}) {
+        if (!tab) continue;
+        Item it;
+        CUDA_TRY(h, cudaMemcpy(&it, tab + item, sizeof(Item), cudaMemcpyDeviceToHost));
+        it.flat_off = flat_off;
+        CUDA_TRY(h, cudaMemcpy(tab + item, &it, sizeof(Item), cudaMemcpyHostToDevice));
+    }
+    return LAMB_OK;
+}
+#endif
 
 extern "C" lamb_status lamb_set_max_ctas(lamb_t h, int32_t max_ctas) {
     if (!h) return fail(nullptr, LAMB_EINVAL, "null handle");

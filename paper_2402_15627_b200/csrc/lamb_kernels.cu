@@ -124,6 +124,22 @@ __device__ __forceinline__ void chunk_a(float4 g, float4& m, float4& v, const fl
     v = make_float4(vv[0], vv[1], vv[2], vv[3]);
 }
 
+// debug: one work item's bounds against the buffers it is streamed from / to
+__device__ __forceinline__ void dcheck_item(const StepParams& P, int64_t ix, const Item& I) {
+    LAMB_DCHECK(ix >= 0 && ix < P.n_items, "item %lld of %lld", (long long)ix, (long long)P.n_items);
+    LAMB_DCHECK(I.n_chunk >= 1 && I.n_chunk <= (int)(kItemElems / 4), "item %lld n_chunk %d", (long long)ix, I.n_chunk);
+    LAMB_DCHECK(I.shard_off % 8 == 0 && I.flat_off % 8 == 0, "item %lld offsets %lld %lld not 8-aligned",
+                (long long)ix, (long long)I.shard_off, (long long)I.flat_off);
+    LAMB_DCHECK(I.shard_off >= 0 && I.shard_off + 4 * (int64_t)I.n_chunk <= P.shard_elems,
+                "item %lld shard range %lld+%d beyond %lld", (long long)ix, (long long)I.shard_off, 4 * I.n_chunk,
+                (long long)P.shard_elems);
+    LAMB_DCHECK(I.flat_off >= 0 && I.flat_off + 4 * (int64_t)I.n_chunk <= P.flat_elems,
+                "item %lld flat range %lld+%d beyond %lld", (long long)ix, (long long)I.flat_off, 4 * I.n_chunk,
+                (long long)P.flat_elems);
+    LAMB_DCHECK(I.tensor >= 0 && I.tensor < P.n_tensors && I.group >= 0 && I.group < LAMB_MAX_GROUPS,
+                "item %lld tensor %d group %d", (long long)ix, I.tensor, I.group);
+}
+
 // ------------------------------------------------------------ pass A
 // NS > 0: NS bf16 sources (fused reduce-scatter, NS = D); NS == 0: fp32 reduced shard (g32).
 // Lane l of the item's warp handles chunks l, l+32, ...; U chunks per lane are loaded before
@@ -138,6 +154,7 @@ __global__ void __launch_bounds__(kThreads, MINB) pass_a_kernel(const __grid_con
     const float gs = P.clip ? P.clip->gs : P.grad_scale;
     for (int64_t it = P.item_begin + gw; it < P.item_end; it += nw) {
         const Item I = P.items[it];
+        dcheck_item(P, it, I);
         const GroupConst G = P.groups[I.group];
         float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
         float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
@@ -221,16 +238,49 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+#ifndef LAMB_DEBUG
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n"
         " mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
         " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)), "r"(phase) : "memory");
 }
+#else
+// debug: the same wait, bounded (20 s) — a ring that never completes is reported, not hung
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+        uint32_t ok;
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok) : "r"(smem_u32(b)), "r"(phase) : "memory");
+        if (ok) return;
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        LAMB_DCHECK(t - t0 < 20000000000ull, "mbarrier at smem 0x%x parity %u never completed", smem_u32(b), phase);
+    }
+}
+#endif
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+
+// debug: per-stage tags of the TMA rings — the producer records which item it filled a stage
+// with (before the arrive that releases the stage), the consumers check it after their wait
+#ifdef LAMB_DEBUG
+#define LAMB_RING_TAGS(name, n) __shared__ int64_t name[n]
+#define LAMB_TAG_SET(name, k, ix) (name)[k] = (ix)
+#define LAMB_TAG_CHECK(name, k, ix)                                                                   \
+    LAMB_DCHECK((name)[k] == (ix), "ring stage %d holds item %lld, consumers expect %lld", (int)(k),  \
+                (long long)(name)[k], (long long)(ix))
+#else
+#define LAMB_RING_TAGS(name, n)
+#define LAMB_TAG_SET(name, k, ix)
+#define LAMB_TAG_CHECK(name, k, ix)
+#endif
 
 // Copy-engine schedule: logical position -> item (reverse walk), and the per-bucket arrival wait
 // of the producer thread (system-scope acquire of the peers' flags, bounded).
@@ -275,6 +325,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
     uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem + sizeof(TmaStage<NS>) * S);
     uint64_t* empty = full + S;
     __shared__ double red_w[kTmaConsumers / 32], red_u[kTmaConsumers / 32];
+    LAMB_RING_TAGS(tag, S);
     const int tid = threadIdx.x;
     if (P.clip && P.clip->skip) return;
     if (tid == 0) {
@@ -297,6 +348,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
                 const int64_t ix = item_at(P, it);
                 wait_bucket_arrivals(P, ix, last_b);
                 const Item I = P.items[ix];
+                dcheck_item(P, ix, I);
+                LAMB_TAG_SET(tag, k, ix);
                 const uint32_t nf = (uint32_t)I.n_chunk * 16u, ng = (uint32_t)I.n_chunk * 8u;
                 mbar_expect_tx(full + k, 3 * nf + NS * ng);
 #pragma unroll
@@ -321,6 +374,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
         const Item I = P.items[ix];
         const GroupConst G = P.groups[I.group];
         mbar_wait(full + k, phase);
+        LAMB_TAG_CHECK(tag, k, ix);
         float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
         float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
         float sw = 0.f, su = 0.f;
@@ -395,6 +449,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
     uint64_t* gfull = empty + SS;
     uint64_t* gempty = gfull + GS;
     __shared__ double red_w[kTmaConsumers / 32], red_u[kTmaConsumers / 32];
+    LAMB_RING_TAGS(gtag, GS);
+    LAMB_RING_TAGS(stag, SS);
     const int tid = threadIdx.x;
     if (P.clip && P.clip->skip) return;
     if (tid == 0) {
@@ -426,6 +482,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
                     const int64_t ix = item_at(P, it);
                     wait_bucket_arrivals(P, ix, last_b);
                     const Item I = P.items[ix];
+                    dcheck_item(P, ix, I);
+                    LAMB_TAG_SET(gtag, kg, ix);
                     const uint32_t ng = (uint32_t)I.n_chunk * 8u;
                     mbar_expect_tx(gfull + kg, NR * ng);
 #pragma unroll
@@ -439,6 +497,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
                 while (si < P.item_end && (!more || si <= it - (int64_t)L * stride)) {
                     mbar_wait(empty + ks, ps ^ 1);
                     const Item I = P.items[item_at(P, si)];
+                    LAMB_TAG_SET(stag, ks, item_at(P, si));
                     const uint32_t nf = (uint32_t)I.n_chunk * 16u, ng = (uint32_t)I.n_chunk * 8u;
                     mbar_expect_tx(full + ks, 3 * nf + (OWN ? ng : 0));
                     bulk_g2s(st[ks].m, P.m + I.shard_off, nf, full + ks);
@@ -463,6 +522,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma2_kernel(cons
         const GroupConst G = P.groups[I.group];
         mbar_wait(gfull + kg, pg);
         mbar_wait(full + ks, ps);
+        LAMB_TAG_CHECK(gtag, kg, ix);
+        LAMB_TAG_CHECK(stag, ks, ix);
         float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
         float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
         float sw = 0.f, su = 0.f;
@@ -543,6 +604,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_nvls_kernel(cons
     uint64_t* full = reinterpret_cast<uint64_t*>(nvls_smem + sizeof(TmaStageS) * S);
     uint64_t* empty = full + S;
     __shared__ double red_w[kTmaConsumers / 32], red_u[kTmaConsumers / 32];
+    LAMB_RING_TAGS(tag, S);
     const int tid = threadIdx.x;
     if (tid == 0) {
         for (int k = 0; k < S; ++k) {
@@ -560,6 +622,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_nvls_kernel(cons
             for (int64_t it = first; it < P.item_end; it += stride) {
                 mbar_wait(empty + k, phase ^ 1);
                 const Item I = P.items[it];
+                dcheck_item(P, it, I);
+                LAMB_TAG_SET(tag, k, it);
                 const uint32_t nf = (uint32_t)I.n_chunk * 16u;
                 mbar_expect_tx(full + k, 3 * nf);
                 bulk_g2s(st[k].m, P.m + I.shard_off, nf, full + k);
@@ -583,6 +647,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_nvls_kernel(cons
         const GroupConst G = P.groups[I.group];
         const int npairs = I.n_chunk >> 1;
         mbar_wait(full + k, phase);
+        LAMB_TAG_CHECK(tag, k, it);
         float4* __restrict__ mp = reinterpret_cast<float4*>(P.m + I.shard_off);
         float4* __restrict__ vp = reinterpret_cast<float4*>(P.v + I.shard_off);
         float sw = 0.f, su = 0.f;
@@ -660,6 +725,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const
     TmaStageB* st = reinterpret_cast<TmaStageB*>(tma_smem_b);
     uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem_b + sizeof(TmaStageB) * kTmaStages);
     uint64_t* empty = full + kTmaStages;
+    LAMB_RING_TAGS(tag, kTmaStages);
     const int tid = threadIdx.x;
     if (P.clip && P.clip->skip) return;
     if (tid == 0) {
@@ -678,6 +744,9 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const
             for (int64_t it = first; it < P.item_end; it += stride) {
                 mbar_wait(empty + k, phase ^ 1);
                 const Item I = P.items[it];
+                dcheck_item(P, it, I);
+                LAMB_DCHECK(I.tensor < P.n_tensors, "scale index %d", I.tensor);
+                LAMB_TAG_SET(tag, k, it);
                 const uint32_t nf = (uint32_t)I.n_chunk * 16u;
                 mbar_expect_tx(full + k, 3 * nf);
                 bulk_g2s(st[k].m, P.m + I.shard_off, nf, full + k);
@@ -696,6 +765,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_b_tma_kernel(const
         const GroupConst G = P.groups[I.group];
         const float scale = P.scale[I.tensor];
         mbar_wait(full + k, phase);
+        LAMB_TAG_CHECK(tag, k, it);
         float4* __restrict__ wp = reinterpret_cast<float4*>(P.w + I.shard_off);
         for (int c = tid; c < I.n_chunk; c += kTmaConsumers) {
             float4 w = st[k].w[c];
@@ -848,6 +918,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_segments_kernel(const __
     const int tid = threadIdx.x;
     if (P.clip && P.clip->skip) return;
     const SegDesc S = P.segs[blockIdx.x];
+    LAMB_DCHECK(S.item_begin >= 0 && S.item_begin <= S.item_end && S.item_end <= P.n_items && S.tensor >= 0 &&
+                    S.tensor < P.n_tensors && S.strad_slot < P.n_strad,
+                "segment %d: items [%lld, %lld) of %lld, tensor %d, straddler slot %d of %d", (int)blockIdx.x,
+                (long long)S.item_begin, (long long)S.item_end, (long long)P.n_items, S.tensor, S.strad_slot, P.n_strad);
     double w2 = 0.0, u2 = 0.0;
     int64_t i = S.item_begin + tid;
     for (; i + 7 * kFinThreads < S.item_end; i += 8 * kFinThreads) {
@@ -894,6 +968,8 @@ __global__ void finalize_straddlers_kernel(const __grid_constant__ FinalizeParam
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= P.n_local_strad || (P.clip && P.clip->skip)) return;
     const int slot = P.strad_slots[k];
+    LAMB_DCHECK(slot >= 0 && slot < P.n_strad && P.strad_tensor[k] < P.n_tensors, "straddler %d slot %d of %d", k, slot,
+                P.n_strad);
     double w2 = 0.0, u2 = 0.0;
     for (int j = 0; j < P.world; ++j) {
         const double2 q = P.xbuf[(int64_t)j * P.n_strad + slot];
@@ -938,6 +1014,13 @@ __global__ void barrier_kernel_v(const __grid_constant__ BarrierArgs A, uint64_t
         __threadfence_system();
         st_release_sys(A.flags[j] + rank, e);
         const uint64_t t0 = globaltimer();
+#ifdef LAMB_DEBUG
+        {   // a peer can be at most one barrier ahead: no barrier completes without every rank
+            const uint64_t seen = ld_acquire_sys(A.flags[rank] + j);
+            LAMB_DCHECK(seen <= e + 1, "barrier epoch %llu: rank %d announced %llu", (unsigned long long)e, j,
+                        (unsigned long long)seen);
+        }
+#endif
         while (ld_acquire_sys(A.flags[rank] + j) < e) {
             if (globaltimer() - t0 > timeout_ns) {
                 atomicExch(err, 1);

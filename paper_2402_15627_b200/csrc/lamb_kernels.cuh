@@ -16,6 +16,27 @@
 
 namespace lamb {
 
+// LAMB_DEBUG build (liblamb_debug.so, paper_2402_15627_b200/build.py): device-side checks in
+// place of compute-sanitizer, which is closed on this GPU pool — item bounds and alignment
+// against the buffers' extents, a tag per ring stage (the item the producer filled must be the
+// one the consumers expect: a ring-phase or early-overwrite error shows up as a mismatch),
+// bounded mbarrier waits (deadlock -> message + trap), segment / straddler / barrier-epoch
+// bounds.  A failed check prints "LAMB_DEBUG ..." and traps.  The release build compiles none of it.
+#ifdef LAMB_DEBUG
+#define LAMB_DCHECK(cond, fmt, ...)                                                            \
+    do {                                                                                       \
+        if (!(cond)) {                                                                         \
+            printf("LAMB_DEBUG %s:%d block %d thread %d: check (%s) failed: " fmt "\n", __FILE__,     \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x, #cond, ##__VA_ARGS__);             \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define LAMB_DCHECK(cond, fmt, ...) \
+    do {                            \
+    } while (0)
+#endif
+
 constexpr int kThreads = 256;          // threads per CTA of the streaming passes
 constexpr int kChunk = 4;              // elements per lane access (16 B fp32, 8 B bf16)
 constexpr int64_t kItemElems = 4096;   // max elements per work item (multiple of 8)
@@ -97,6 +118,9 @@ struct StepParams {
     // param buffers (one address reaches the same offset on every rank through the NVSwitch)
     const __nv_bfloat16* gmc;   // pass A: multimem.ld_reduce (switch-side fp32 sum, bf16 result)
     __nv_bfloat16* pmc;         // pass B: multimem.st (one store lands in every rank's buffer)
+    // extents, checked by the LAMB_DEBUG build only (bounds of every item it touches)
+    int64_t shard_elems, flat_elems, n_items;
+    int32_t n_tensors;
 };
 
 struct FinalizeParams {
@@ -120,6 +144,8 @@ struct FinalizeParams {
     const double2* xbuf;            // this rank's exchange buffer
     const ClipState* clip;          // skip flag (pre-step)
     const GroupConst* groups;       // device table [n_groups]
+    int64_t n_items;                // extents, checked by the LAMB_DEBUG build only
+    int32_t n_tensors;
 };
 
 // Per-step constants of every group, written to device memory by one tiny kernel launched on

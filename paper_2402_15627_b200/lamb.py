@@ -13,7 +13,11 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblamb.so")
+# LAMB_DEBUG_LIB=1 loads the -DLAMB_DEBUG build (device-side bounds / ring-tag / bounded-wait
+# checks standing in for compute-sanitizer): same kernels and arithmetic, so the
+# results are the same; a failed check prints "LAMB_DEBUG ..." and traps
+DEBUG = os.environ.get("LAMB_DEBUG_LIB", "0") not in ("", "0")
+LIB_PATH = os.path.join(_HERE, "liblamb_debug.so" if DEBUG else "liblamb.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2402_15627_b200.build` "
@@ -121,6 +125,8 @@ _SIGS = {
                                ctypes.c_uint32, _vp]),
     "lamb_synth_philox": (_st, [_vp, _vp, _vp]),
 }
+if DEBUG:
+    _SIGS["lamb_debug_corrupt_item"] = (_st, [_vp, ctypes.c_int64, ctypes.c_int64])
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_L, _name)
     _f.restype = _res

@@ -804,6 +804,8 @@ def main():
     rank = int(os.environ["RANK"])
     local = int(os.environ["LOCAL_RANK"])
     from paper_2402_15627_b200 import lamb
+    if rank == 0:
+        print(f"[lib] {lamb.LIB_PATH}", flush=True)
     mode = {"fused": lamb.LAMB_COMM_FUSED, "nccl": lamb.LAMB_COMM_NCCL, "nvls": lamb.LAMB_COMM_NVLS}[a.mode]
 
     if a.oversub:

@@ -118,3 +118,20 @@ def test_binding_fails_loudly_without_the_library(tmp_path):
     mod = importlib.util.module_from_spec(spec)
     with pytest.raises(ImportError, match="no CPU fallback"):
         spec.loader.exec_module(mod)
+
+
+def test_debug_build_exports_its_hooks_and_carries_the_checks(L):
+    # liblamb_debug.so (-DLAMB_DEBUG): the release ABI plus lamb_debug.h's hook, and device-side
+    # checks (trap sites) that the release library does not contain
+    import subprocess
+    dbg = B.build(debug=True)
+    so = ctypes.CDLL(dbg)
+    for n in declared_functions():
+        assert hasattr(so, n), n
+    assert hasattr(so, "lamb_debug_corrupt_item")
+    assert not hasattr(ctypes.CDLL(B.build()), "lamb_debug_corrupt_item")
+
+    def traps(path):
+        sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
+        return sass.count("BPT.TRAP")
+    assert traps(dbg) > 50 and traps(B.build()) == 0

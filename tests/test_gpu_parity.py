@@ -21,6 +21,7 @@ def lamb():
     from paper_2402_15627_b200 import build
     build.build()
     from paper_2402_15627_b200 import lamb as L
+    print(f"[lib] {L.LIB_PATH}", flush=True)
     return L
 
 
