@@ -248,6 +248,26 @@ def nvls_ckpt_case(world, rank, local, mode):
     dist.barrier()
 
 
+def nvls_refused_case(world, rank, local):
+    """NVLS needs one GPU per rank (multicast objects bind one allocation per device): with ranks
+    sharing GPUs, lamb_create fails with LAMB_EUNSUPPORTED on EVERY rank (the status byte of each
+    setup phase is all-gathered) instead of leaving some ranks waiting."""
+    from paper_2402_15627_b200 import lamb
+    if world <= torch.cuda.device_count():
+        return
+    wl = W.toy()
+    try:
+        lamb.Lamb([(t.numel, t.group) for t in wl.tensors], wl.groups, world_size=world, rank=rank, device=local,
+                  comm_mode=lamb.LAMB_COMM_NVLS, pg=dist.group.WORLD, bootstrap=BOOT)
+        raise AssertionError("NVLS accepted ranks that share a GPU")
+    except lamb.LambError as e:
+        assert e.status == lamb.LAMB_EUNSUPPORTED and "share a GPU" in str(e), str(e)
+    dist.barrier()
+    if rank == 0:
+        print(f"[ok] NVLS refused on every rank when {world} ranks share {torch.cuda.device_count()} GPU(s)",
+              flush=True)
+
+
 def clip_case(world, rank, local, mode):
     """Pre-step at D ranks: the global norm spans every rank's shard; clipping active; then a
     non-finite gradient on one rank makes every rank skip."""
@@ -835,6 +855,7 @@ def main():
         ce_rollback_case(world, rank, local, mode)
         torch_case(world, rank, local, mode)
         torch_overlap_case(world, rank, local, mode)
+        nvls_refused_case(world, rank, local)
         dist.barrier()
         dist.destroy_process_group()
         return
