@@ -349,7 +349,7 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
     struct PeerRec {
         cudaIpcMemHandle_t ipc[4];
         void* raw[4];
-        int64_t pid;
+        uint64_t process;   // process identity: random per process (pids repeat across containers)
         int32_t device, pad;
     };
     PeerRec mine;
@@ -361,7 +361,12 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
         CUDA_TRY(h, cudaIpcGetMemHandle(&mine.ipc[k], bufs[k]));
         mine.raw[k] = bufs[k];
     }
-    mine.pid = (int64_t)getpid();
+    static const uint64_t process_token = [] {
+        std::random_device rd;
+        return ((uint64_t)rd() << 32) ^ (uint64_t)rd() ^ ((uint64_t)getpid() << 20) ^
+               (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count();
+    }();
+    mine.process = process_token;
     mine.device = h->device;
     std::vector<PeerRec> all((size_t)D);
     {
@@ -370,7 +375,7 @@ static lamb_status setup_comm(lamb_ctx* h, const uint8_t* id) {
     }
     for (int j = 0; j < D; ++j) {
         if (j == r) continue;
-        const bool local = all[j].pid == mine.pid;
+        const bool local = all[j].process == mine.process;
         if (local && all[j].device != h->device) {
             const cudaError_t e = cudaDeviceEnablePeerAccess(all[j].device, 0);
             if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
