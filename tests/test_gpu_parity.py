@@ -97,6 +97,34 @@ def test_group_variants(lamb):
     L.close()
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_random_hyperparameters_property(lamb, seed):
+    """Property sweep (SPEC-style randomized small configs): random ragged tables under random
+    groups — beta1 in [0.5, 0.99), beta2 in [0.9, 0.9999), eps in [1e-9, 1e-4], weight decay in
+    [0, 0.3], lr a power of two in [2^-12, 2^-6], adapt / bias correction on or off, a random
+    bucket cap — 1-3 steps, element-wise against the oracle with the per-step update check."""
+    rng = np.random.default_rng(1000 + seed)
+    n_groups = int(rng.integers(1, 5))
+    groups = [W.GroupSpec(lr=2.0 ** -int(rng.integers(6, 13)), beta1=float(np.float32(rng.uniform(0.5, 0.99))),
+                          beta2=float(np.float32(rng.uniform(0.9, 0.9999))),
+                          eps=float(np.float32(10.0 ** rng.uniform(-9, -4))),
+                          weight_decay=float(np.float32(rng.uniform(0, 0.3))) if rng.random() < 0.7 else 0.0,
+                          adapt=int(rng.random() < 0.8), bias_correction=int(rng.random() < 0.8))
+              for _ in range(n_groups)]
+    tensors = W.random_table(rng, int(rng.integers(5, 40)), max_numel=6000, p_big=0.2, big=60_000)
+    tensors = [W.TensorSpec(t.name, t.numel, int(rng.integers(0, n_groups)), t.init, t.gexp) for t in tensors]
+    wl = W.Workload("prop", 40 + seed, tensors, groups)
+    steps = int(rng.integers(1, 4))
+    L = run_gpu(wl, steps=steps, cap=int(rng.integers(2000, 80_000)))
+    orc = oracle.OracleRun(wl, world_size=1)
+    for t in range(1, steps + 1):
+        orc.step(t)
+    compare_state(L, orc, steps)
+    print(f"seed {seed}: {len(tensors)} tensors, {n_groups} groups, {steps} steps, "
+          f"update check max |err|/allowed = {L.update_worst:.3f}")
+    L.close()
+
+
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 def test_two_devices_in_one_process(lamb):
     """Handles on two GPUs in one process (lamb.h: several handles per process): the
