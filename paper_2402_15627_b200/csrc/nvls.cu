@@ -148,6 +148,12 @@ bool recv_fds(int listener, int timeout_ms, int* from, std::vector<int>* fds, st
     if (poll(&p, 1, timeout_ms) != 1) return *why = "timed out waiting for a peer's descriptors", false;
     const int c = accept4(listener, nullptr, nullptr, SOCK_CLOEXEC);
     if (c < 0) return *why = "accept()", false;
+    ucred cred;
+    socklen_t clen = sizeof(cred);
+    if (getsockopt(c, SOL_SOCKET, SO_PEERCRED, &cred, &clen) != 0 || cred.uid != getuid()) {
+        close(c);   // only processes of this user may hand us memory
+        return *why = "descriptor message from another user", false;
+    }
     FdMsg m{-1, 0};
     iovec io{&m, sizeof(m)};
     std::vector<char> ctl(CMSG_SPACE(sizeof(int) * 8));
