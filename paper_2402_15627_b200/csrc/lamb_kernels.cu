@@ -17,9 +17,10 @@
 // complete_tx; for D > 1 the bulk copies pull the peers' gradient slices over NVLink), eight
 // consumer warps compute and store with 16 B streaming STGs (profiles/r01_tma.md: 99.3 % /
 // 102.5 % of the measured HBM copy bandwidth at D = 1).  At D = 2 pass A keeps the peers'
-// slices in a separate, deeper ring (pass_a_tma2_kernel).  The LDG/STG kernels (128-bit
-// coalesced ld/st.global.cs, several chunks per lane in flight, profiles/r01_final.md) remain
-// as LAMB_TUNE variants and serve the NCCL-mode fp32 input.
+// slices in a separate, deeper ring (pass_a_tma2_kernel).  The LDG kernel (128-bit coalesced
+// ld/st.global.cs, several chunks per lane in flight, profiles/r01_final.md) serves the
+// NCCL-mode / pre-step fp32 input.  NVLS mode: pass_a_nvls_kernel (multimem.ld_reduce) and
+// pass_b_tma_kernel<1, true> (multimem.st).
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -215,8 +216,7 @@ __device__ __forceinline__ float4 sum_raw(const uint2 (&raw)[NS]) {
 // ------------------------------------------------------------ pass A, TMA variant (default, any D)
 // One producer warp stages whole items (g 8 B, m/v/w 16 B per 4-element chunk) into a 3-stage
 // shared-memory ring with 1-D bulk copies (cp.async.bulk, TMA engine; mbarrier complete_tx);
-// 8 consumer warps compute from shared memory and store m, v with 16 B STGs.  Tunable
-// (LAMB_TUNE tma=1) against the LDG kernel.
+// 8 consumer warps compute from shared memory and store m, v with 16 B STGs.
 constexpr int kTmaStages = 3;
 constexpr int kTmaConsumers = 256;
 constexpr int kTmaItem = (int)kItemElems;   // elements per stage (one item)
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32, 1) pass_a_tma_kernel(const
 // the item's m/v/w (SS-stage ring): the remote reads, whose latency the single ring exposed at
 // D = 2 (pass A 90 % of HBM vs 99 % with local-only sources), get a deep prefetch without
 // duplicating the state ring.  OWN: this rank's local slice rides in the state ring, only the
-// NS - 1 remote slices in the deep ring.  Tunable (LAMB_TUNE tmam=2..5).
+// NS - 1 remote slices in the deep ring.  Default at D = 2 (LAMB_TUNE tmam=0|1 for A/B timing).
 template <int NR>
 struct TmaGradStage {
     uint2 g[NR][kTmaItem / 4];
