@@ -41,6 +41,11 @@ FALLBACK_HBM_GBS = 6650.0
 NVLINK_PEER_GBS = 770.0
 NVLINK_PULL_GBS = NVLINK_PEER_GBS
 NVLINK_PUSH_GBS = NVLINK_PEER_GBS
+# Context for the NVLink fractions: what an all-to-all actually reaches on this fabric (no
+# compute, per GPU, user data) — TMA bulk pulls 658-669 GB/s at D = 4 (tools/p2p_bench.cu mode 1,
+# profiles/r02/p2p_tma_pull_D4_D2.jsonl), STG pushes 695-700 GB/s (profiles/r01/p2p_all2all_D4.json)
+ALLTOALL_PULL_GBS = 669.0
+ALLTOALL_PUSH_GBS = 700.0
 CURVE_CONFIG = "175b_slice_3l"     # north_star: "1->8 GPU step-time scaling curve on the 175B-slice layout"
 
 
@@ -492,7 +497,12 @@ class Run:
             roof = {"bound": "nvlink", "kernel": dom["kernel"], "achieved": dom["nvlink_GBps"],
                     "peak": dom["nvlink_peak"], "unit": "GB/s", "frac": dom["nvlink_frac"],
                     "traffic": traffic,
-                    "peak_source": "B200_PROFILING.md measured peer copy, 770 GB/s per direction per GPU"}
+                    "peak_source": "B200_PROFILING.md measured peer copy, 770 GB/s per direction per GPU",
+                    "alltoall_ceiling": {"GBps": ALLTOALL_PULL_GBS if dom["kernel"] == "pass_a" else ALLTOALL_PUSH_GBS,
+                                         "frac": dom["nvlink_GBps"] / (ALLTOALL_PULL_GBS if dom["kernel"] == "pass_a"
+                                                                      else ALLTOALL_PUSH_GBS),
+                                         "source": "measured all-to-all (no compute) on this pool: TMA pulls / "
+                                                   "STG pushes, DESIGN.md §11b"}}
         else:
             roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["GBps"], "peak": hbm,
                     "unit": "GB/s", "frac": dom["hbm_frac"], "traffic": traffic, "peak_source": hbm_src}
