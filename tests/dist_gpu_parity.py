@@ -816,6 +816,8 @@ def main():
     ap.add_argument("--full", action="store_true",
                     help="only the full-size BASELINE configs: 530B+stress (all stress tensors and "
                          "LayerNorm tensors checked) and 13B (sampled), in the bench launch config")
+    ap.add_argument("--quick", action="store_true",
+                    help="with --oversub: only the parity cases (toy, toy10, ragged, stress, H8 replicated)")
     ap.add_argument("--oversub", action="store_true",
                     help="D ranks on fewer GPUs (rank %% GPUs), host bootstrap, gloo: the D-rank FUSED "
                          "kernels and protocol (e.g. D = 8) on a smaller box")
@@ -843,6 +845,11 @@ def main():
         stress = W.stress_tensors(0, 3000)
         run_case("stress", W.Workload("stress", 51, stress, W.default_groups()), world, rank, local, mode, 2,
                  cap=100_000)
+        if a.quick:
+            replicated_case(world, rank, local, mode)
+            dist.barrier()
+            dist.destroy_process_group()
+            return
         ckpt_case(world, rank, local, mode)
         clip_case(world, rank, local, mode)
         bucket_case(world, rank, local, mode)

@@ -72,3 +72,12 @@ def test_parity_8ranks_oversubscribed():
     kernels, the 8-rank barrier/straddler protocol and the FUSED checkpoint reload, bootstrapped
     without NCCL through lamb_create_with_allgather over a gloo group."""
     _torchrun(8, "--mode", "fused", "--oversub", timeout=1200)
+
+
+@pytest.mark.skipif(NGPU < 1, reason="needs a GPU")
+@pytest.mark.parametrize("world", [5, 6, 7])
+def test_parity_odd_worlds_oversubscribed(world):
+    """D = 5, 6, 7 (the NS = ND = 5..7 pass kernels, Q = 128 lcm(D, 8) layouts, inexact
+    grad_scale = 1/D) on whatever GPUs the box has, against the oracle: toy, 10 steps, ragged,
+    stress straddlers and H8 (replicated gradients == the unsharded D = 1 oracle)."""
+    _torchrun(world, "--mode", "fused", "--oversub", "--quick", timeout=900)
