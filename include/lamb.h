@@ -129,11 +129,15 @@ lamb_status lamb_get_unique_id(uint8_t id[LAMB_UNIQUE_ID_BYTES]);
 
 /* COLLECTIVE.  Plans, allocates (library-owned: flat bf16 grad and param buffers, zeroed;
  * fp32 w/m/v shards), creates the NCCL communicator and, in LAMB_COMM_FUSED, maps every
- * peer's grad/param/exchange buffers over NVLink (CUDA IPC).  `id` may be NULL when D = 1.
+ * peer's grad/param/exchange buffers over NVLink (CUDA IPC; peer access for ranks of the same
+ * process); in LAMB_COMM_NVLS the grad/param buffers are multicast-bound VMM allocations
+ * (csrc/nvls.cu).  `id` may be NULL when D = 1.
  * EINVAL: see lamb_plan_create, n_groups not in [1, LAMB_MAX_GROUPS], group out of range,
  * bad hyper-parameters, reserved != 0, or (D > 1) another rank passed a different table /
  * config (a hash is all-gathered and compared; every rank fails).  ENOMEM, ECUDA, ENCCL,
- * EUNSUPPORTED (device not sm_100, or peers not NVLink-reachable in FUSED mode).
+ * EUNSUPPORTED (device not sm_100, peers not NVLink-reachable in FUSED mode, an unknown
+ * comm_mode, LAMB_FLAG_CE with NVLS, or in NVLS mode: no multicast support or ranks sharing a
+ * GPU — then on every rank).
  * Failure detection: every cross-GPU wait is bounded by LAMB_BARRIER_TIMEOUT_MS (environment,
  * default 30000); a peer that does not arrive makes the next call return LAMB_ECUDA, after
  * which the handle must be destroyed. */
