@@ -193,16 +193,34 @@ def cpu_baseline(wl, seconds: float) -> dict:
     return out
 
 
+def run_config(args, wl, world: int, flat_size: int) -> dict:
+    """The `config` object of the JSON line — identical for our arm and the reference arm (the
+    reference times a bounded sample of this same workload; the sample is described in its
+    cpu_baseline)."""
+    return {"workload": wl.name, "n_params": wl.n_params, "n_tensors": len(wl.tensors),
+            "flat_size": flat_size, "world_size": world,
+            "comm": args.comm if world > 1 else "none", "bucket_cap": wl.cap,
+            "prestep_clip": args.clip if args.clip > 0 else None,
+            "cuda_graph": bool(args.graph), "max_ctas": args.max_ctas or None,
+            "l2": "inputs larger than L2 (fp32 state of the shard >> 126 MB)",
+            "io_dtype": "bf16 grads in / bf16 params out, fp32 master and moments",
+            "parallelism": f"zero2-dp{world}"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import oracle
     wl = W.get(args.config)
     v, ms, cores, desc, k = oracle_sample(wl, 0, max_steps=args.steps, warmup=args.warmup)
+    flat = oracle.plan([t.numel for t in wl.tensors], args.gpus, wl.cap).flat_size   # oracle planner
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl.name, "sample": desc},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Philox4x32-10 grads/weights, DESIGN.md §4); the CPU oracle (double) on a "
+                    "bounded sample of the workload: " + desc,
+            "config": run_config(args, wl, args.gpus, flat),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
                              "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -676,14 +694,7 @@ def main():
             "steps": K, "warmup": Wm, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Philox4x32-10 grads/weights, DESIGN.md §4)",
-            "config": {"workload": wl.name, "n_params": wl.n_params, "n_tensors": len(wl.tensors),
-                       "flat_size": main_line["flat"], "world_size": world,
-                       "comm": args.comm if world > 1 else "none", "bucket_cap": wl.cap,
-                       "prestep_clip": args.clip if args.clip > 0 else None,
-                       "cuda_graph": bool(args.graph), "max_ctas": args.max_ctas or None,
-                       "l2": "inputs larger than L2 (fp32 state of the shard >> 126 MB)",
-                       "io_dtype": "bf16 grads in / bf16 params out, fp32 master and moments",
-                       "parallelism": f"zero2-dp{world}"},
+            "config": run_config(args, wl, world, main_line["flat"]),
             "ranks_seen": n_seen,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": main_line["launches"],
             "host_enqueue_us_per_step": main_line["host_us"],

@@ -31,3 +31,19 @@ def test_reference_arm_other_ranks_exit_quietly():
                        env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip() == ""
+
+
+def test_reference_arm_config_is_our_arms_config():
+    # the driver compares the two arms' `config`: the reference line carries our arm's config for
+    # the same arguments (flat_size from the oracle planner == the library planner's, H12)
+    sys.path.insert(0, ROOT)
+    import bench
+    import workloads as W
+    from paper_2402_15627_b200 import lamb
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    ref = json.loads(r.stdout.strip().splitlines()[-1])
+    wl = W.get("gpt1.3b")
+    pv = lamb.host_plan([t.numel for t in wl.tensors], 1, 0, wl.cap)
+    ours = bench.run_config(bench.parse([]), wl, 1, int(pv.flat_size))
+    assert ref["config"] == ours
