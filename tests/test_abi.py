@@ -135,3 +135,17 @@ def test_debug_build_exports_its_hooks_and_carries_the_checks(L):
         sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
         return sass.count("BPT.TRAP")
     assert traps(dbg) > 50 and traps(B.build()) == 0
+
+
+def _compile_c_example(L, out):
+    import subprocess
+    lib_dir = os.path.dirname(L.LIB_PATH if not L.DEBUG else B.build())
+    return subprocess.run(["gcc", "-std=c11", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "lamb_c_example.c"), "-o", out, "-L", lib_dir, "-llamb",
+                           f"-Wl,-rpath,{lib_dir}", "-lm"], capture_output=True, text=True)
+
+
+def test_c_example_compiles_against_the_headers(L, tmp_path):
+    # the boundary is plain C: the example builds with gcc against include/*.h and liblamb.so alone
+    r = _compile_c_example(L, str(tmp_path / "lamb_c_example"))
+    assert r.returncode == 0, r.stderr

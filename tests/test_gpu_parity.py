@@ -14,6 +14,7 @@ torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module")
@@ -718,3 +719,28 @@ def test_set_master_from_host_needs_one_bucket_of_device_memory(lamb):
         assert torch.equal(p[lo:lo + 4096].cpu(), x[lo:lo + 4096].bfloat16())
     del ballast
     L.close()
+
+
+def test_c_example_matches_the_oracle(lamb, tmp_path):
+    """examples/lamb_c_example.c — the C ABI from plain C (no Python in the step path): its trust
+    ratios and first master weights after two toy steps equal the oracle's."""
+    import re
+    import subprocess
+    lib_dir = os.path.dirname(lamb.LIB_PATH)
+    exe = str(tmp_path / "lamb_c_example")
+    r = subprocess.run(["gcc", "-std=c11", "-O2", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "lamb_c_example.c"), "-o", exe, "-L", lib_dir, "-llamb",
+                        f"-Wl,-rpath,{lib_dir}", "-lm"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    orc = oracle.OracleRun(W.toy(), world_size=1)
+    orc.step(1)
+    orc.step(2)
+    ratios = [float(x) for x in re.findall(r"trust ratio = ([0-9.eE+-]+)", r.stdout)]
+    assert len(ratios) == 3
+    for i, got in enumerate(ratios):
+        assert abs(got - orc.stats[i][2]) <= 1e-5 * abs(orc.stats[i][2]) + 1e-6, (i, got, orc.stats[i])
+    w = [float(x) for x in re.search(r"w\[0\.\.3\] = (\S+) (\S+) (\S+) (\S+)", r.stdout).groups()]
+    for k in range(4):   # printed with 8 decimals
+        assert abs(w[k] - orc.w[0][k]) <= 1e-8 + 1e-5 * abs(orc.w[0][k]), (k, w[k], orc.w[0][k])
